@@ -1,0 +1,200 @@
+/*
+ * wrng_gpu.h — C ABI of the B200 (sm_100a) Wallace normal generator.
+ *
+ * This is the drop-in boundary for the reference's generator interface
+ * (/root/reference/proj/include/wrng/wallace.hpp).  Every entry point below
+ * replaces one reference member / free function, cited as file:line.  No C++
+ * types, exceptions or torch types cross it: plain pointers, sizes and status
+ * codes.  include/wrng_gpu/wallace.hpp wraps it back into the reference's C++
+ * API (WallaceConfig / WallaceState, same exception types).
+ *
+ * Generalisations over the reference (all default to the reference's
+ * behaviour: n_arrays = 2, dtype = f64, pools = 1):
+ *   - n_arrays = 4: Wallace's 4x4 orthogonal variant (docs/n4_spec.md);
+ *   - dtype = f32 pools (all per-pass scalars still computed in f64);
+ *   - pools = P independent generators in one handle ("bank"); pool p is
+ *     the reference state (seed, stream_id + p) (uniform.cpp:23-26).  A fill
+ *     of `count` values writes pool p's stream into the contiguous segment of
+ *     count/P (+1 for p < count % P) values starting at sum of the previous
+ *     segments ("pool-major").
+ *
+ * Threading: a handle is single-owner (wallace.hpp:113-114); distinct handles
+ * may be used concurrently from different host threads.
+ */
+#ifndef WRNG_GPU_H
+#define WRNG_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WRNG_GPU_ABI_VERSION 1
+
+/* Status codes.  Map 1:1 onto the reference's exceptions:
+ *   EINVAL     std::invalid_argument      (wallace.cpp:141-149, 199;
+ *                                           uniform.cpp:48-49)
+ *   ECORRUPT   wrng::corrupted_state_error (errors.hpp:10-13;
+ *                                           wallace.cpp:59-61, 229-232)
+ *   EMALFORMED_* wrng::malformed_state_error{kind} (errors.hpp:15-32;
+ *                                           serialize.cpp:63-66, 76-78, 117-169)
+ *   ECUDA / ENOMEM / ENODEV: device-side failures (no reference analogue). */
+typedef enum wrng_gpu_status {
+    WRNG_GPU_OK = 0,
+    WRNG_GPU_EINVAL = 1,
+    WRNG_GPU_ECORRUPT = 2,
+    WRNG_GPU_EMALFORMED_BAD_MAGIC = 3,
+    WRNG_GPU_EMALFORMED_VERSION = 4,
+    WRNG_GPU_EMALFORMED_TRUNCATED = 5,
+    WRNG_GPU_EMALFORMED_FIELD_RANGE = 6,
+    WRNG_GPU_ECUDA = 7,
+    WRNG_GPU_ENOMEM = 8,
+    WRNG_GPU_ENODEV = 9
+} wrng_gpu_status;
+
+enum { WRNG_GPU_F64 = 0, WRNG_GPU_F32 = 1 };
+enum { WRNG_GPU_CHISQ = 0, WRNG_GPU_FIXED = 1 }; /* ScaleMode, wallace.hpp:52-55 */
+
+/* Config flags. */
+enum {
+    /* Initial pool from the host (glibc libm) instead of the device
+     * Box-Muller kernel: bit-identical to the reference's init_pool
+     * (wallace.cpp:158-167).  The device path agrees to a few ulp. */
+    WRNG_GPU_INIT_HOST = 1u << 0,
+    /* Engine selection (default: shared-memory pools when a pool fits in
+     * one CTA's shared memory, else HBM-resident double-buffered pools). */
+    WRNG_GPU_FORCE_HBM = 1u << 1,
+    /* drift_check by a fast parallel reduction instead of the reference's
+     * left-to-right order (Pool::direct_sumsq, wallace.hpp:44-46).  Off by
+     * default: the default path reproduces the sequential sum bit-exactly. */
+    WRNG_GPU_DRIFT_TREE = 1u << 2
+};
+
+/* WallaceConfig (wallace.hpp:57-65) + the B200 extensions. */
+typedef struct wrng_gpu_config {
+    uint32_t pool_exponent;           /* N = 2^p per array, p in [8, 20] */
+    uint32_t throwaway_f;             /* >= 1: passes per exposed pool */
+    uint32_t scale_mode;              /* WRNG_GPU_CHISQ | WRNG_GPU_FIXED */
+    uint32_t n_arrays;                /* 2 (reference) or 4 */
+    uint64_t restart_interval_passes; /* 0 = never, else > throwaway_f */
+    uint64_t drift_check_period;      /* passes between audits, 0 = never */
+    uint64_t seed;
+    uint64_t stream_id;               /* pool p uses stream_id + p */
+    uint32_t dtype;                   /* WRNG_GPU_F64 | WRNG_GPU_F32 */
+    uint32_t pools;                   /* >= 1 independent pools */
+    int32_t device;                   /* CUDA device ordinal */
+    uint32_t flags;                   /* WRNG_GPU_* flags */
+} wrng_gpu_config;
+
+/* PassParams (wallace.hpp:22-30), flattened for n in {2, 4}.
+ * n = 2: stride = {alpha, beta}, offset = {gamma, delta}, (c, s) = rot.
+ * n = 4: stride[0..3], offset[0..3], variant in {0, 1} (docs/n4_spec.md). */
+typedef struct wrng_gpu_params {
+    uint32_t stride[4];
+    uint32_t offset[4];
+    uint32_t variant;
+    uint32_t pad_;
+    double c;
+    double s;
+    double scale;
+    double target_sumsq;
+} wrng_gpu_params;
+
+typedef struct wrng_gpu_counters {
+    uint64_t pass_count;      /* WallaceState::pass_count (wallace.hpp:150) */
+    uint64_t numbers_emitted; /* WallaceState::numbers_emitted (:151) */
+    uint64_t avail;           /* WallaceState::avail (:152) */
+    uint32_t active;          /* double-buffer flag (wallace.hpp:168) */
+    uint32_t pool_size;       /* N (wallace.hpp:149) */
+} wrng_gpu_counters;
+
+typedef struct wrng_gpu wrng_gpu_t;
+
+/* Reference defaults: p = 10, f = 3, chisq, no restart, drift 64, seed 0,
+ * stream 0 (wallace.hpp:57-65); n = 2, f64, 1 pool, device 0, no flags. */
+void wrng_gpu_config_default(wrng_gpu_config* cfg);
+
+/* WallaceState::WallaceState (wallace.cpp:139-156): validates, seeds each
+ * pool's uniform generator (uniform.cpp:23-32) and fills the initial pools
+ * (wallace.cpp:158-167).  EINVAL on a bad config. */
+wrng_gpu_status wrng_gpu_create(const wrng_gpu_config* cfg, wrng_gpu_t** out);
+void wrng_gpu_destroy(wrng_gpu_t* g);
+
+/* WallaceState::fill (wallace.cpp:198-216), every pool, pool-major output.
+ * out_is_device != 0: `out` is device memory and the work is enqueued on
+ * `stream` (a cudaStream_t, NULL = legacy default) without a host sync; a
+ * device-detected ECORRUPT is returned by the next synchronising call.
+ * out_is_device == 0: `out` is host memory (pinned or pageable); generation
+ * is overlapped with the device-to-host copies and the call returns when all
+ * values are in `out`.  sigma < 0 -> EINVAL (wallace.cpp:199). */
+wrng_gpu_status wrng_gpu_fill_f64(wrng_gpu_t* g, double* out, uint64_t count,
+                                  double mu, double sigma, int out_is_device,
+                                  void* stream);
+wrng_gpu_status wrng_gpu_fill_f32(wrng_gpu_t* g, float* out, uint64_t count,
+                                  double mu, double sigma, int out_is_device,
+                                  void* stream);
+
+/* WallaceState::advance_pass (wallace.cpp:169-178) on every pool; the
+ * parameters used are written to params[p] when params != NULL. */
+wrng_gpu_status wrng_gpu_advance_pass(wrng_gpu_t* g, wrng_gpu_params* params);
+/* WallaceState::refill (wallace.cpp:188-196) on every pool. */
+wrng_gpu_status wrng_gpu_refill(wrng_gpu_t* g);
+/* WallaceState::drift_check (wallace.cpp:225-234) on every pool. */
+wrng_gpu_status wrng_gpu_drift_check(wrng_gpu_t* g);
+/* WallaceState::restart (wallace.cpp:236) on every pool. */
+wrng_gpu_status wrng_gpu_restart(wrng_gpu_t* g);
+
+/* Accessors (wallace.hpp:148-160). */
+wrng_gpu_status wrng_gpu_get_config(const wrng_gpu_t* g, wrng_gpu_config* out);
+wrng_gpu_status wrng_gpu_get_counters(const wrng_gpu_t* g, uint32_t pool,
+                                      wrng_gpu_counters* out);
+/* active_pool() (wallace.hpp:156-157): values (n_arrays * N, array-major,
+ * widened to double), tracked_sumsq, withheld. */
+wrng_gpu_status wrng_gpu_read_pool(wrng_gpu_t* g, uint32_t pool, double* values,
+                                   double* tracked_sumsq, double* withheld);
+/* Mutable active_pool(): overwrite the live pool (tests model callers that
+ * scribble over the work area, test_wallace_state.cpp:128-150). */
+wrng_gpu_status wrng_gpu_write_pool(wrng_gpu_t* g, uint32_t pool, const double* values,
+                                    double tracked_sumsq, double withheld);
+/* uniform_state() (wallace.hpp:158): lag table, cursors, draws. */
+wrng_gpu_status wrng_gpu_read_uniform(wrng_gpu_t* g, uint32_t pool, uint64_t* table607,
+                                      uint32_t* cursor_r, uint32_t* cursor_s,
+                                      uint64_t* draws);
+
+/* save_state / load_state (serialize.cpp:82-169).  A handle with n = 2,
+ * f64, 1 pool exports the reference's "WRNG" v1 bytes exactly; anything else
+ * exports v2 (docs/n4_spec.md §6).  export: *size receives the byte count;
+ * bytes are copied only when cap >= *size (buf may be NULL to query). */
+wrng_gpu_status wrng_gpu_export_state(wrng_gpu_t* g, uint8_t* buf, size_t cap,
+                                      size_t* size);
+wrng_gpu_status wrng_gpu_import_state(const uint8_t* bytes, size_t size, int32_t device,
+                                      uint32_t flags, wrng_gpu_t** out);
+
+/* Blocks until the handle's queued work is done; reports device errors. */
+wrng_gpu_status wrng_gpu_synchronize(wrng_gpu_t* g);
+/* Message of the handle's last failing call ("" when none). */
+const char* wrng_gpu_last_error(const wrng_gpu_t* g);
+/* Number of this library's kernels launched by the handle so far. */
+uint64_t wrng_gpu_kernel_launches(const wrng_gpu_t* g);
+/* Name of the engine the handle runs: "smem" or "hbm". */
+const char* wrng_gpu_engine(const wrng_gpu_t* g);
+
+/* Validation reductions on device data: n, m1..m4
+ * from per-block fp64 partial sums (tree order).  Synchronous. */
+wrng_gpu_status wrng_gpu_moments_f32(const float* dev, uint64_t n, double* out5,
+                                     int32_t device, void* stream);
+wrng_gpu_status wrng_gpu_moments_f64(const double* dev, uint64_t n, double* out5,
+                                     int32_t device, void* stream);
+
+/* Device uniform generator, for bit-exact stream checks: the first `count`
+ * next_word() outputs of UniformState(seed, stream_id + p) for p < pools,
+ * pool-major (uniform.cpp:23-40). */
+wrng_gpu_status wrng_gpu_lfg_words(uint64_t seed, uint64_t stream_id, uint32_t pools,
+                                   uint64_t count, uint64_t* host_out, int32_t device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WRNG_GPU_H */

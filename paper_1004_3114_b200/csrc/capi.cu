@@ -1,0 +1,1143 @@
+// extern "C" implementation of include/wrng_gpu.h.
+//
+// Host-side control for the two engines (kernels.cu), the counter mirror,
+// host-output staging (generation overlapped with D2H copies), the optional
+// host (glibc) initial pool, and state import/export in the reference's
+// "WRNG" v1 format (serialize.cpp:6-13) plus our v2 for n = 4 / f32 / banks.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace wg;
+
+namespace {
+
+struct Ctr {  // per-pool counter mirror (WallaceState, wallace.hpp:167-172)
+    uint64_t pc = 0, avail = 0, emitted = 0;
+    uint32_t active = 0;
+};
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+bool crossed(uint64_t before, uint64_t after, uint64_t period) {
+    return period > 0 && after / period > before / period;  // wallace.cpp:182-184
+}
+
+}  // namespace
+
+struct wrng_gpu {
+    wrng_gpu_config cfg{};
+    uint32_t N = 0;
+    uint64_t nvals = 0, cap = 0;
+    size_t esize = 8;
+    bool hbm = false;
+    void* buf[2] = {nullptr, nullptr};
+    PoolMeta* meta = nullptr;
+    LfgState* lfg = nullptr;
+    wrng_gpu_params* params = nullptr;  // device: per-pool param records / hbm batches
+    size_t params_cap = 0;
+    double* scratch = nullptr;
+    cudaStream_t stream = nullptr;       // internal stream
+    cudaStream_t copy_stream = nullptr;  // D2H of staged host fills
+    cudaStream_t last = nullptr;         // last stream work was queued on
+    bool last_set = false;
+    cudaEvent_t order_ev = nullptr;
+    void* stage[2] = {nullptr, nullptr};
+    size_t stage_bytes = 0;
+    cudaEvent_t gen_done[2] = {nullptr, nullptr}, copy_done[2] = {nullptr, nullptr};
+    std::vector<Ctr> ctr;
+    uint64_t launches = 0;
+    std::string err;
+};
+
+namespace {
+
+wrng_gpu_status fail(wrng_gpu* g, wrng_gpu_status s, const std::string& what) {
+    if (g) g->err = what;
+    return s;
+}
+
+wrng_gpu_status cuda_fail(wrng_gpu* g, cudaError_t e, const char* where) {
+    return fail(g, WRNG_GPU_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr)                                                   \
+    do {                                                           \
+        cudaError_t e_ = (expr);                                   \
+        if (e_ != cudaSuccess) return cuda_fail(g, e_, #expr);     \
+    } while (0)
+
+#define LAUNCH(expr)                                               \
+    do {                                                           \
+        cudaError_t e_ = (expr);                                   \
+        if (e_ != cudaSuccess) return cuda_fail(g, e_, #expr);     \
+        ++g->launches;                                             \
+    } while (0)
+
+// Orders work on stream `s` after everything queued so far on the handle.
+wrng_gpu_status order_on(wrng_gpu* g, cudaStream_t s) {
+    if (g->last_set && g->last != s) {
+        CK(cudaEventRecord(g->order_ev, g->last));
+        CK(cudaStreamWaitEvent(s, g->order_ev, 0));
+    }
+    g->last = s;
+    g->last_set = true;
+    return WRNG_GPU_OK;
+}
+
+KernelArgs base_args(const wrng_gpu* g) {
+    KernelArgs a{};
+    a.buf[0] = g->buf[0];
+    a.buf[1] = g->buf[1];
+    a.meta = g->meta;
+    a.lfg = g->lfg;
+    a.N = g->N;
+    a.f = g->cfg.throwaway_f;
+    a.mode = g->cfg.scale_mode;
+    a.pools = g->cfg.pools;
+    a.restart = g->cfg.restart_interval_passes;
+    a.drift = g->cfg.drift_check_period;
+    a.seed = g->cfg.seed;
+    a.stream0 = g->cfg.stream_id;
+    a.mu = 0.0;
+    a.sigma = 1.0;
+    a.unit = 1;
+    return a;
+}
+
+KernelArgs pool_args(const wrng_gpu* g, uint32_t p) {
+    KernelArgs a = base_args(g);
+    a.buf[0] = static_cast<char*>(g->buf[0]) + (size_t)p * g->nvals * g->esize;
+    a.buf[1] = static_cast<char*>(g->buf[1]) + (size_t)p * g->nvals * g->esize;
+    a.meta = g->meta + p;
+    a.lfg = g->lfg + p;
+    a.stream0 = g->cfg.stream_id + p;
+    a.pools = 1;
+    return a;
+}
+
+// Pulls device meta; on any device-raised error, resynchronises the counter
+// mirror from the device, clears the flags and reports the error.
+wrng_gpu_status collect(wrng_gpu* g) {
+    CK(cudaStreamSynchronize(g->stream));
+    if (g->last_set && g->last != g->stream) CK(cudaStreamSynchronize(g->last));
+    CK(cudaStreamSynchronize(g->copy_stream));
+    const uint32_t P = g->cfg.pools;
+    std::vector<PoolMeta> m(P);
+    CK(cudaMemcpy(m.data(), g->meta, sizeof(PoolMeta) * P, cudaMemcpyDeviceToHost));
+    uint32_t code = 0;
+    for (uint32_t p = 0; p < P; ++p) {
+        if (m[p].error) {
+            code = m[p].error;
+            m[p].error = 0;
+        }
+    }
+    if (!code) return WRNG_GPU_OK;
+    for (uint32_t p = 0; p < P; ++p) {
+        g->ctr[p].pc = m[p].pass_count;
+        g->ctr[p].avail = m[p].avail;
+        g->ctr[p].emitted = m[p].emitted;
+        g->ctr[p].active = m[p].active;
+    }
+    CK(cudaMemcpy(g->meta, m.data(), sizeof(PoolMeta) * P, cudaMemcpyHostToDevice));
+    return fail(g, (wrng_gpu_status)code,
+                "corrupted_state_error: tracked sum of squares not positive, or the "
+                "drift audit found the pool sum of squares off by more than 1e-3");
+}
+
+// ---- host-side plan (mirror of the smem kernel's control flow) -----------
+struct Ev {
+    enum Kind { EMIT, PASS, DRIFT, RESTART } kind;
+    uint64_t pos = 0, take = 0, out_off = 0, emit_n = 0;
+    uint32_t end_refill = 0;
+};
+
+void plan_fill(const wrng_gpu* g, Ctr& c, uint64_t len, std::vector<Ev>* ev) {
+    const uint64_t cap = g->cap, f = g->cfg.throwaway_f;
+    const uint64_t R = g->cfg.restart_interval_passes, D = g->cfg.drift_check_period;
+    uint64_t done = 0;
+    if (c.avail > 0 && len > 0) {
+        uint64_t take = std::min(len, c.avail);
+        if (ev) {
+            Ev e{Ev::EMIT};
+            e.pos = cap - c.avail;
+            e.take = take;
+            e.out_off = 0;
+            ev->push_back(e);
+        }
+        done = take;
+        c.avail -= take;
+    }
+    while (done < len) {
+        const uint64_t before = c.pc;
+        const bool will_restart = R > 0 && crossed(before, before + f, R);
+        const uint64_t emit_n = will_restart ? 0 : std::min(len - done, cap);
+        for (uint64_t i = 0; i < f; ++i) {
+            if (ev) {
+                Ev e{Ev::PASS};
+                e.emit_n = i + 1 == f ? emit_n : 0;
+                e.out_off = done;
+                e.end_refill = i + 1 == f;
+                ev->push_back(e);
+            }
+            ++c.pc;
+            c.active ^= 1u;
+        }
+        c.avail = cap;
+        if (crossed(before, c.pc, D) && ev) ev->push_back(Ev{Ev::DRIFT});
+        if (will_restart) {
+            if (ev) ev->push_back(Ev{Ev::RESTART});
+            c.avail = 0;
+            continue;
+        }
+        done += emit_n;
+        c.avail -= emit_n;
+    }
+    c.emitted += len;
+}
+
+void plan_refill(const wrng_gpu* g, Ctr& c, std::vector<Ev>* ev) {
+    const uint64_t f = g->cfg.throwaway_f;
+    const uint64_t before = c.pc;
+    for (uint64_t i = 0; i < f; ++i) {
+        if (ev) {
+            Ev e{Ev::PASS};
+            e.end_refill = i + 1 == f;
+            ev->push_back(e);
+        }
+        ++c.pc;
+        c.active ^= 1u;
+    }
+    c.avail = g->cap;
+    if (crossed(before, c.pc, g->cfg.drift_check_period) && ev) ev->push_back(Ev{Ev::DRIFT});
+    if (g->cfg.restart_interval_passes > 0 &&
+        crossed(before, c.pc, g->cfg.restart_interval_passes)) {
+        if (ev) ev->push_back(Ev{Ev::RESTART});
+        c.avail = 0;
+    }
+}
+
+wrng_gpu_status ensure_params(wrng_gpu* g, size_t n) {
+    if (n <= g->params_cap) return WRNG_GPU_OK;
+    if (g->params) cudaFree(g->params);
+    g->params = nullptr;
+    size_t want = std::max<size_t>(n, 1024);
+    CK(cudaMalloc(&g->params, want * sizeof(wrng_gpu_params)));
+    g->params_cap = want;
+    return WRNG_GPU_OK;
+}
+
+// Executes a plan on HBM pool p (host-driven: one launch per pass).
+wrng_gpu_status run_hbm(wrng_gpu* g, uint32_t p, Ctr c, const std::vector<Ev>& ev,
+                        KernelArgs a, cudaStream_t s) {
+    const uint32_t NA = g->cfg.n_arrays, dt = g->cfg.dtype;
+    size_t i = 0;
+    while (i < ev.size()) {
+        // batch the parameter draws of consecutive passes (restart draws
+        // uniforms for Box-Muller and therefore splits batches)
+        size_t jend = i;
+        while (jend < ev.size() && ev[jend].kind != Ev::RESTART) ++jend;
+        uint32_t npass = 0;
+        for (size_t k = i; k < jend; ++k) npass += ev[k].kind == Ev::PASS;
+        if (npass) {
+            wrng_gpu_status st = ensure_params(g, npass);
+            if (st) return st;
+            LAUNCH(launch_hbm_params(NA, g->N, a.lfg, g->params, npass, a.meta, s));
+        }
+        uint32_t pi = 0;
+        for (size_t k = i; k < jend; ++k) {
+            const Ev& e = ev[k];
+            if (e.kind == Ev::EMIT) {
+                LAUNCH(launch_hbm_emit(NA, dt, a, c.active, e.pos, e.take, e.out_off, s));
+            } else if (e.kind == Ev::PASS) {
+                HbmPass ps{};
+                ps.src = c.active;
+                ps.param_idx = pi++;
+                ps.emit_n = e.emit_n;
+                ps.out_off = e.out_off;
+                ps.end_refill = e.end_refill;
+                LAUNCH(launch_hbm_pass(NA, dt, a, g->params, ps, s));
+                c.active ^= 1u;
+            } else if (e.kind == Ev::DRIFT) {
+                LAUNCH(launch_hbm_drift(NA, dt, a, c.active,
+                                        (g->cfg.flags & WRNG_GPU_DRIFT_TREE) != 0, g->scratch,
+                                        s));
+            }
+        }
+        if (jend < ev.size()) {  // RESTART
+            LAUNCH(launch_hbm_init(NA, dt, a, c.active, 0, s));
+            ++jend;
+        }
+        i = jend;
+    }
+    (void)p;
+    return WRNG_GPU_OK;
+}
+
+// One device-output bank fill (no staging): `lay` places each pool's values.
+wrng_gpu_status fill_device(wrng_gpu* g, void* out, int out_f32, const OutLayout& lay,
+                            double mu, double sigma, cudaStream_t s) {
+    const uint32_t P = g->cfg.pools;
+    const bool unit = mu == 0.0 && sigma == 1.0;
+    wrng_gpu_status st = order_on(g, s);
+    if (st) return st;
+    if (!g->hbm) {
+        KernelArgs a = base_args(g);
+        a.op = OP_FILL;
+        a.out = out;
+        a.out_f32 = out_f32;
+        a.unit = unit;
+        a.mu = mu;
+        a.sigma = sigma;
+        a.lay = lay;
+        LAUNCH(launch_smem(g->cfg.n_arrays, g->cfg.dtype, a, s));
+        for (uint32_t p = 0; p < P; ++p)
+            plan_fill(g, g->ctr[p], lay.len_base + (p < lay.len_extra ? 1 : 0), nullptr);
+        return WRNG_GPU_OK;
+    }
+    const size_t esz = out_f32 ? 4 : 8;
+    for (uint32_t p = 0; p < P; ++p) {
+        const uint64_t len = lay.len_base + (p < lay.len_extra ? 1 : 0);
+        if (len == 0) continue;
+        const uint64_t off = (uint64_t)p * lay.off_stride + std::min<uint64_t>(p, lay.off_extra);
+        KernelArgs a = pool_args(g, p);
+        a.out = static_cast<char*>(out) + off * esz;
+        a.out_f32 = out_f32;
+        a.unit = unit;
+        a.mu = mu;
+        a.sigma = sigma;
+        std::vector<Ev> ev;
+        Ctr before = g->ctr[p];
+        plan_fill(g, g->ctr[p], len, &ev);
+        st = run_hbm(g, p, before, ev, a, s);
+        if (st) return st;
+        const Ctr& c = g->ctr[p];
+        LAUNCH(launch_hbm_setmeta(a.meta, c.pc, c.avail, c.emitted, c.active, s));
+    }
+    return WRNG_GPU_OK;
+}
+
+wrng_gpu_status ensure_stage(wrng_gpu* g) {
+    if (g->stage[0]) return WRNG_GPU_OK;
+    g->stage_bytes = (size_t)256 << 20;
+    for (int b = 0; b < 2; ++b) {
+        CK(cudaMalloc(&g->stage[b], g->stage_bytes));
+        CK(cudaEventCreateWithFlags(&g->gen_done[b], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g->copy_done[b], cudaEventDisableTiming));
+        CK(cudaEventRecord(g->copy_done[b], g->copy_stream));
+    }
+    return WRNG_GPU_OK;
+}
+
+// Host-output fill: generation into two device slabs alternating with
+// asynchronous D2H copies; pool p's segment stays contiguous in `out`.
+wrng_gpu_status fill_host(wrng_gpu* g, void* out, int out_f32, uint64_t count, double mu,
+                          double sigma, cudaStream_t s) {
+    wrng_gpu_status st = ensure_stage(g);
+    if (st) return st;
+    const uint32_t P = g->cfg.pools;
+    const size_t esz = out_f32 ? 4 : 8;
+    const uint64_t base = count / P, extra = count % P;
+    const uint64_t stage_elems = g->stage_bytes / esz;
+    char* hout = static_cast<char*>(out);
+    int b = 0;
+    if (!g->hbm) {
+        // Sub-chunk t covers stream positions [t, t + L) of every pool's
+        // segment; the chunk that reaches the shorter segments' end is the
+        // tail (pools p < extra hold one value more).
+        const uint64_t L = std::max<uint64_t>(1, stage_elems / P);
+        for (uint64_t t = 0;; t += L) {
+            const bool tail = t + L > base;
+            OutLayout lay{};
+            lay.off_stride = L;
+            lay.off_extra = 0;
+            lay.len_base = tail ? base - t : L;
+            lay.len_extra = tail ? extra : 0;
+            const uint64_t wb = lay.len_base, we = lay.len_base + (tail ? 1 : 0);
+            if (wb == 0 && (extra == 0 || !tail)) break;
+            CK(cudaStreamWaitEvent(s, g->copy_done[b], 0));
+            st = fill_device(g, g->stage[b], out_f32, lay, mu, sigma, s);
+            if (st) return st;
+            CK(cudaEventRecord(g->gen_done[b], s));
+            CK(cudaStreamWaitEvent(g->copy_stream, g->gen_done[b], 0));
+            if (extra > 0 && we > 0)  // pools [0, extra): segment pitch base + 1
+                CK(cudaMemcpy2DAsync(hout + t * esz, (base + 1) * esz, g->stage[b], L * esz,
+                                     we * esz, extra, cudaMemcpyDeviceToHost,
+                                     g->copy_stream));
+            if (P > extra && wb > 0)  // pools [extra, P): segment pitch base
+                CK(cudaMemcpy2DAsync(hout + (extra * (base + 1) + t) * esz, base * esz,
+                                     static_cast<char*>(g->stage[b]) + extra * L * esz,
+                                     L * esz, wb * esz, P - extra, cudaMemcpyDeviceToHost,
+                                     g->copy_stream));
+            CK(cudaEventRecord(g->copy_done[b], g->copy_stream));
+            b ^= 1;
+            if (tail) break;
+        }
+    } else {
+        for (uint32_t p = 0; p < P; ++p) {
+            const uint64_t len = base + (p < extra ? 1 : 0);
+            const uint64_t off = (uint64_t)p * base + std::min<uint64_t>(p, extra);
+            for (uint64_t t = 0; t < len; t += stage_elems) {
+                const uint64_t c = std::min<uint64_t>(stage_elems, len - t);
+                CK(cudaStreamWaitEvent(s, g->copy_done[b], 0));
+                // single-pool fill of c values into the slab
+                KernelArgs a = pool_args(g, p);
+                a.out = g->stage[b];
+                a.out_f32 = out_f32;
+                a.unit = mu == 0.0 && sigma == 1.0;
+                a.mu = mu;
+                a.sigma = sigma;
+                st = order_on(g, s);
+                if (st) return st;
+                std::vector<Ev> ev;
+                Ctr before = g->ctr[p];
+                plan_fill(g, g->ctr[p], c, &ev);
+                st = run_hbm(g, p, before, ev, a, s);
+                if (st) return st;
+                const Ctr& cc = g->ctr[p];
+                LAUNCH(launch_hbm_setmeta(a.meta, cc.pc, cc.avail, cc.emitted, cc.active, s));
+                CK(cudaEventRecord(g->gen_done[b], s));
+                CK(cudaStreamWaitEvent(g->copy_stream, g->gen_done[b], 0));
+                CK(cudaMemcpyAsync(hout + (off + t) * esz, g->stage[b], c * esz,
+                                   cudaMemcpyDeviceToHost, g->copy_stream));
+                CK(cudaEventRecord(g->copy_done[b], g->copy_stream));
+                b ^= 1;
+            }
+        }
+    }
+    CK(cudaStreamSynchronize(g->copy_stream));
+    return collect(g);
+}
+
+wrng_gpu_status do_fill(wrng_gpu* g, void* out, int out_f32, uint64_t count, double mu,
+                        double sigma, int out_is_device, void* stream) {
+    if (!g) return WRNG_GPU_EINVAL;
+    if (sigma < 0.0) return fail(g, WRNG_GPU_EINVAL, "fill: sigma must be >= 0");
+    if (count > 0 && !out) return fail(g, WRNG_GPU_EINVAL, "fill: null output");
+    DeviceGuard dg(g->cfg.device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
+    if (count == 0) {
+        for (auto& c : g->ctr) plan_fill(g, c, 0, nullptr);
+        return WRNG_GPU_OK;
+    }
+    if (!out_is_device) return fill_host(g, out, out_f32, count, mu, sigma, s);
+    const uint32_t P = g->cfg.pools;
+    OutLayout lay{count / P, count % P, count / P, count % P};
+    return fill_device(g, out, out_f32, lay, mu, sigma, s);
+}
+
+// Runs an op on every pool (smem: one launch; hbm: per pool) and syncs.
+wrng_gpu_status run_op(wrng_gpu* g, Op op, wrng_gpu_params* params_host) {
+    DeviceGuard dg(g->cfg.device);
+    wrng_gpu_status st = order_on(g, g->stream);
+    if (st) return st;
+    const uint32_t P = g->cfg.pools;
+    if (op == OP_PASSES && params_host) {
+        st = ensure_params(g, P);
+        if (st) return st;
+    }
+    if (!g->hbm) {
+        KernelArgs a = base_args(g);
+        a.op = op;
+        a.npasses = 1;
+        a.params_out = (op == OP_PASSES && params_host) ? g->params : nullptr;
+        LAUNCH(launch_smem(g->cfg.n_arrays, g->cfg.dtype, a, g->stream));
+        for (uint32_t p = 0; p < P; ++p) {
+            Ctr& c = g->ctr[p];
+            if (op == OP_PASSES) {
+                ++c.pc;
+                c.active ^= 1u;
+                c.avail = 0;
+            } else if (op == OP_REFILL) {
+                plan_refill(g, c, nullptr);
+            } else if (op == OP_RESTART) {
+                c.avail = 0;
+            }
+        }
+    } else {
+        for (uint32_t p = 0; p < P; ++p) {
+            KernelArgs a = pool_args(g, p);
+            Ctr& c = g->ctr[p];
+            if (op == OP_PASSES) {
+                LAUNCH(launch_hbm_params(g->cfg.n_arrays, g->N, a.lfg, g->params + p, 1, a.meta,
+                                         g->stream));
+                HbmPass ps{};
+                ps.src = c.active;
+                ps.param_idx = 0;
+                LAUNCH(launch_hbm_pass(g->cfg.n_arrays, g->cfg.dtype, a, g->params + p, ps,
+                                       g->stream));
+                ++c.pc;
+                c.active ^= 1u;
+                c.avail = 0;
+            } else if (op == OP_REFILL) {
+                std::vector<Ev> ev;
+                Ctr before = c;
+                plan_refill(g, c, &ev);
+                st = run_hbm(g, p, before, ev, a, g->stream);
+                if (st) return st;
+                LAUNCH(launch_hbm_setmeta(a.meta, c.pc, c.avail, c.emitted, c.active, g->stream));
+            } else if (op == OP_DRIFT) {
+                LAUNCH(launch_hbm_drift(g->cfg.n_arrays, g->cfg.dtype, a, c.active,
+                                        (g->cfg.flags & WRNG_GPU_DRIFT_TREE) != 0, g->scratch,
+                                        g->stream));
+            } else if (op == OP_RESTART) {
+                LAUNCH(launch_hbm_init(g->cfg.n_arrays, g->cfg.dtype, a, c.active, 0, g->stream));
+                c.avail = 0;
+            }
+        }
+    }
+    st = collect(g);
+    if (op == OP_PASSES && params_host && st == WRNG_GPU_OK)
+        CK(cudaMemcpy(params_host, g->params, sizeof(wrng_gpu_params) * P,
+                      cudaMemcpyDeviceToHost));
+    return st;
+}
+
+// ---- host (glibc) initial pool: bit-identical to init_pool --------------
+struct HostLfg {
+    uint64_t t[kTable];
+    uint32_t r = 0;
+    uint64_t draws = 0;
+    void seed(uint64_t seed, uint64_t stream) {  // uniform.cpp:23-32
+        uint64_t s = seed ^ ((stream << 32) | (stream >> 32));
+        for (uint32_t i = 0; i < kTable; ++i) {
+            s += 0x9E3779B97F4A7C15ull;
+            uint64_t z = s;
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            t[i] = z ^ (z >> 31);
+        }
+        r = 0;
+        for (uint32_t i = 0; i < kWarmup; ++i) word();
+        draws = 0;
+    }
+    uint64_t word() {  // uniform.cpp:34-40
+        uint32_t s = r + kGap;
+        if (s >= kTable) s -= kTable;
+        uint64_t w = t[r] + t[s];
+        t[r] = w;
+        if (++r == kTable) r = 0;
+        return w;
+    }
+    double uniform() {  // uniform.cpp:42-45
+        ++draws;
+        return (double)(word() >> 11) * 0x1.0p-53;
+    }
+};
+
+void host_box_muller(HostLfg& u, double& x, double& y) {  // reference.cpp:9-22
+    double u1 = u.uniform();
+    if (u1 == 0.0) u1 = 0x1.0p-53;
+    double u2 = u.uniform();
+    const double pi = 3.141592653589793;
+    double radius = std::sqrt(-2.0 * std::log(u1));
+    double angle = 2.0 * pi * u2;
+    x = radius * std::cos(angle);
+    y = radius * std::sin(angle);
+}
+
+wrng_gpu_status host_init(wrng_gpu* g) {
+    const uint32_t P = g->cfg.pools;
+    std::vector<char> vals(g->nvals * g->esize);
+    std::vector<LfgState> lfg(P);
+    std::vector<PoolMeta> meta(P);
+    for (uint32_t p = 0; p < P; ++p) {
+        HostLfg u;
+        u.seed(g->cfg.seed, g->cfg.stream_id + p);
+        const double zero = 0.0;
+        for (uint64_t i = 0; i < g->nvals; i += 2) {
+            double x, y;
+            host_box_muller(u, x, y);
+            double vx = zero + x, vy = zero + y;  // mu + sigma * z, mu = 0, sigma = 1
+            if (g->cfg.dtype == WRNG_GPU_F64) {
+                reinterpret_cast<double*>(vals.data())[i] = vx;
+                reinterpret_cast<double*>(vals.data())[i + 1] = vy;
+            } else {
+                reinterpret_cast<float*>(vals.data())[i] = (float)vx;
+                reinterpret_cast<float*>(vals.data())[i + 1] = (float)vy;
+            }
+        }
+        double wx, wy;
+        host_box_muller(u, wx, wy);
+        double q = 0.0;
+        for (uint64_t i = 0; i < g->nvals; ++i) {
+            double d = g->cfg.dtype == WRNG_GPU_F64 ? reinterpret_cast<double*>(vals.data())[i]
+                                                    : (double)reinterpret_cast<float*>(vals.data())[i];
+            q = q + d * d;
+        }
+        std::memcpy(lfg[p].table, u.t, sizeof(u.t));
+        lfg[p].r = u.r;
+        lfg[p].draws = u.draws;
+        meta[p] = PoolMeta{};
+        meta[p].tracked[0] = q;
+        meta[p].withheld[0] = wx;
+        CK(cudaMemcpy(static_cast<char*>(g->buf[0]) + (size_t)p * vals.size(), vals.data(),
+                      vals.size(), cudaMemcpyHostToDevice));
+    }
+    CK(cudaMemcpy(g->lfg, lfg.data(), sizeof(LfgState) * P, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(g->meta, meta.data(), sizeof(PoolMeta) * P, cudaMemcpyHostToDevice));
+    return WRNG_GPU_OK;
+}
+
+wrng_gpu_status validate(const wrng_gpu_config* c, bool check_restart) {
+    if (c->pool_exponent < 8 || c->pool_exponent > 20) return WRNG_GPU_EINVAL;
+    if (c->throwaway_f < 1) return WRNG_GPU_EINVAL;
+    if (check_restart && c->restart_interval_passes > 0 &&
+        c->restart_interval_passes <= c->throwaway_f)
+        return WRNG_GPU_EINVAL;
+    if (c->n_arrays != 2 && c->n_arrays != 4) return WRNG_GPU_EINVAL;
+    if (c->dtype > 1 || c->scale_mode > 1 || c->pools < 1) return WRNG_GPU_EINVAL;
+    return WRNG_GPU_OK;
+}
+
+// Allocates a handle without initialising pool contents.
+wrng_gpu_status alloc_handle(const wrng_gpu_config* cfg, wrng_gpu** out) {
+    wrng_gpu* g = new wrng_gpu;
+    g->cfg = *cfg;
+    g->N = 1u << cfg->pool_exponent;
+    g->nvals = (uint64_t)cfg->n_arrays * g->N;
+    g->cap = g->nvals - 1;
+    g->esize = cfg->dtype == WRNG_GPU_F64 ? 8 : 4;
+    g->hbm = (cfg->flags & WRNG_GPU_FORCE_HBM) || !smem_engine_fits(cfg->n_arrays, cfg->dtype, g->N);
+    g->ctr.assign(cfg->pools, Ctr{});
+    *out = g;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(g, WRNG_GPU_ENODEV, "no CUDA device");
+    if (cfg->device < 0 || cfg->device >= ndev) return fail(g, WRNG_GPU_ENODEV, "bad device");
+    DeviceGuard dg(cfg->device);
+    const size_t pool_bytes = (size_t)cfg->pools * g->nvals * g->esize;
+    for (int b = 0; b < 2; ++b) {
+        if (cudaMalloc(&g->buf[b], pool_bytes) != cudaSuccess)
+            return fail(g, WRNG_GPU_ENOMEM, "pool allocation failed");
+        CK(cudaMemset(g->buf[b], 0, pool_bytes));
+    }
+    CK(cudaMalloc(&g->meta, sizeof(PoolMeta) * cfg->pools));
+    CK(cudaMemset(g->meta, 0, sizeof(PoolMeta) * cfg->pools));
+    CK(cudaMalloc(&g->lfg, sizeof(LfgState) * cfg->pools));
+    CK(cudaMalloc(&g->scratch, sizeof(double) * 1024));
+    CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&g->order_ev, cudaEventDisableTiming));
+    return WRNG_GPU_OK;
+}
+
+// ---- serialization helpers ----------------------------------------------
+constexpr uint32_t kMagic = 0x57524E47;  // "WRNG" (serialize.cpp:20)
+
+struct Writer {
+    std::vector<uint8_t> b;
+    void u8(uint8_t v) { b.push_back(v); }
+    void u32(uint32_t v) {
+        for (int i = 0; i < 4; ++i) b.push_back((uint8_t)(v >> (8 * i)));
+    }
+    void u64(uint64_t v) {
+        for (int i = 0; i < 8; ++i) b.push_back((uint8_t)(v >> (8 * i)));
+    }
+    void f64(double v) {
+        uint64_t u;
+        std::memcpy(&u, &v, 8);
+        u64(u);
+    }
+    void raw(const void* p, size_t n) {
+        const uint8_t* c = static_cast<const uint8_t*>(p);
+        b.insert(b.end(), c, c + n);
+    }
+};
+
+struct Reader {
+    const uint8_t* p;
+    size_t n, pos = 0;
+    bool ok = true;
+    bool take(size_t k) {
+        if (!ok || n - pos < k) {
+            ok = false;
+            return false;
+        }
+        return true;
+    }
+    uint8_t u8() {
+        if (!take(1)) return 0;
+        return p[pos++];
+    }
+    uint32_t u32() {
+        if (!take(4)) return 0;
+        uint32_t v = 0;
+        for (int i = 0; i < 4; ++i) v |= (uint32_t)p[pos + i] << (8 * i);
+        pos += 4;
+        return v;
+    }
+    uint64_t u64() {
+        if (!take(8)) return 0;
+        uint64_t v = 0;
+        for (int i = 0; i < 8; ++i) v |= (uint64_t)p[pos + i] << (8 * i);
+        pos += 8;
+        return v;
+    }
+    double f64() {
+        uint64_t u = u64();
+        double d;
+        std::memcpy(&d, &u, 8);
+        return d;
+    }
+    bool raw(void* dst, size_t k) {
+        if (!take(k)) return false;
+        std::memcpy(dst, p + pos, k);
+        pos += k;
+        return true;
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+void wrng_gpu_config_default(wrng_gpu_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->pool_exponent = 10;
+    c->throwaway_f = 3;
+    c->scale_mode = WRNG_GPU_CHISQ;
+    c->n_arrays = 2;
+    c->restart_interval_passes = 0;
+    c->drift_check_period = 64;
+    c->seed = 0;
+    c->stream_id = 0;
+    c->dtype = WRNG_GPU_F64;
+    c->pools = 1;
+    c->device = 0;
+    c->flags = 0;
+}
+
+wrng_gpu_status wrng_gpu_create(const wrng_gpu_config* cfg, wrng_gpu_t** out) {
+    if (!cfg || !out) return WRNG_GPU_EINVAL;
+    *out = nullptr;
+    wrng_gpu_status st = validate(cfg, true);
+    if (st) return st;
+    wrng_gpu* g = nullptr;
+    st = alloc_handle(cfg, &g);
+    if (st) {
+        wrng_gpu_destroy(g);
+        return st;
+    }
+    DeviceGuard dg(cfg->device);
+    if (cfg->flags & WRNG_GPU_INIT_HOST) {
+        st = host_init(g);
+    } else if (!g->hbm) {
+        KernelArgs a = base_args(g);
+        a.op = OP_INIT;
+        cudaError_t e = launch_smem(cfg->n_arrays, cfg->dtype, a, g->stream);
+        st = e == cudaSuccess ? WRNG_GPU_OK : cuda_fail(g, e, "init");
+        ++g->launches;
+    } else {
+        for (uint32_t p = 0; p < cfg->pools && !st; ++p) {
+            KernelArgs a = pool_args(g, p);
+            cudaError_t e = launch_hbm_init(cfg->n_arrays, cfg->dtype, a, 0, 1, g->stream);
+            st = e == cudaSuccess ? WRNG_GPU_OK : cuda_fail(g, e, "init");
+            ++g->launches;
+        }
+    }
+    if (!st) st = collect(g);
+    if (st) {
+        wrng_gpu_destroy(g);
+        return st;
+    }
+    *out = g;
+    return WRNG_GPU_OK;
+}
+
+void wrng_gpu_destroy(wrng_gpu_t* g) {
+    if (!g) return;
+    {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) == cudaSuccess && g->cfg.device >= 0 &&
+            g->cfg.device < ndev) {
+            DeviceGuard dg(g->cfg.device);
+            if (g->stream) cudaStreamSynchronize(g->stream);
+            if (g->copy_stream) cudaStreamSynchronize(g->copy_stream);
+            for (int b = 0; b < 2; ++b) {
+                if (g->buf[b]) cudaFree(g->buf[b]);
+                if (g->stage[b]) cudaFree(g->stage[b]);
+                if (g->gen_done[b]) cudaEventDestroy(g->gen_done[b]);
+                if (g->copy_done[b]) cudaEventDestroy(g->copy_done[b]);
+            }
+            if (g->meta) cudaFree(g->meta);
+            if (g->lfg) cudaFree(g->lfg);
+            if (g->params) cudaFree(g->params);
+            if (g->scratch) cudaFree(g->scratch);
+            if (g->order_ev) cudaEventDestroy(g->order_ev);
+            if (g->stream) cudaStreamDestroy(g->stream);
+            if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
+        }
+    }
+    delete g;
+}
+
+wrng_gpu_status wrng_gpu_fill_f64(wrng_gpu_t* g, double* out, uint64_t count, double mu,
+                                  double sigma, int out_is_device, void* stream) {
+    return do_fill(g, out, 0, count, mu, sigma, out_is_device, stream);
+}
+
+wrng_gpu_status wrng_gpu_fill_f32(wrng_gpu_t* g, float* out, uint64_t count, double mu,
+                                  double sigma, int out_is_device, void* stream) {
+    return do_fill(g, out, 1, count, mu, sigma, out_is_device, stream);
+}
+
+wrng_gpu_status wrng_gpu_advance_pass(wrng_gpu_t* g, wrng_gpu_params* params) {
+    if (!g) return WRNG_GPU_EINVAL;
+    if (g->hbm && !params) {
+        wrng_gpu_status st = ensure_params(g, g->cfg.pools);
+        if (st) return st;
+    }
+    return run_op(g, OP_PASSES, params);
+}
+
+wrng_gpu_status wrng_gpu_refill(wrng_gpu_t* g) {
+    if (!g) return WRNG_GPU_EINVAL;
+    if (g->hbm) {
+        wrng_gpu_status st = ensure_params(g, g->cfg.throwaway_f);
+        if (st) return st;
+    }
+    return run_op(g, OP_REFILL, nullptr);
+}
+
+wrng_gpu_status wrng_gpu_drift_check(wrng_gpu_t* g) {
+    if (!g) return WRNG_GPU_EINVAL;
+    return run_op(g, OP_DRIFT, nullptr);
+}
+
+wrng_gpu_status wrng_gpu_restart(wrng_gpu_t* g) {
+    if (!g) return WRNG_GPU_EINVAL;
+    return run_op(g, OP_RESTART, nullptr);
+}
+
+wrng_gpu_status wrng_gpu_get_config(const wrng_gpu_t* g, wrng_gpu_config* out) {
+    if (!g || !out) return WRNG_GPU_EINVAL;
+    *out = g->cfg;
+    return WRNG_GPU_OK;
+}
+
+wrng_gpu_status wrng_gpu_get_counters(const wrng_gpu_t* g, uint32_t pool,
+                                      wrng_gpu_counters* out) {
+    if (!g || !out || pool >= g->cfg.pools) return WRNG_GPU_EINVAL;
+    const Ctr& c = g->ctr[pool];
+    out->pass_count = c.pc;
+    out->numbers_emitted = c.emitted;
+    out->avail = c.avail;
+    out->active = c.active;
+    out->pool_size = g->N;
+    return WRNG_GPU_OK;
+}
+
+wrng_gpu_status wrng_gpu_read_pool(wrng_gpu_t* g, uint32_t pool, double* values,
+                                   double* tracked, double* withheld) {
+    if (!g || pool >= g->cfg.pools) return WRNG_GPU_EINVAL;
+    DeviceGuard dg(g->cfg.device);
+    wrng_gpu_status st = collect(g);
+    if (st) return st;
+    PoolMeta m;
+    CK(cudaMemcpy(&m, g->meta + pool, sizeof(m), cudaMemcpyDeviceToHost));
+    const uint32_t act = m.active;
+    if (values) {
+        std::vector<char> raw(g->nvals * g->esize);
+        CK(cudaMemcpy(raw.data(), static_cast<char*>(g->buf[act]) + (size_t)pool * raw.size(),
+                      raw.size(), cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < g->nvals; ++i)
+            values[i] = g->esize == 8 ? reinterpret_cast<double*>(raw.data())[i]
+                                      : (double)reinterpret_cast<float*>(raw.data())[i];
+    }
+    if (tracked) *tracked = m.tracked[act];
+    if (withheld) *withheld = m.withheld[act];
+    return WRNG_GPU_OK;
+}
+
+wrng_gpu_status wrng_gpu_write_pool(wrng_gpu_t* g, uint32_t pool, const double* values,
+                                    double tracked, double withheld) {
+    if (!g || pool >= g->cfg.pools) return WRNG_GPU_EINVAL;
+    DeviceGuard dg(g->cfg.device);
+    wrng_gpu_status st = collect(g);
+    if (st) return st;
+    PoolMeta m;
+    CK(cudaMemcpy(&m, g->meta + pool, sizeof(m), cudaMemcpyDeviceToHost));
+    const uint32_t act = m.active;
+    if (values) {
+        std::vector<char> raw(g->nvals * g->esize);
+        for (uint64_t i = 0; i < g->nvals; ++i) {
+            if (g->esize == 8)
+                reinterpret_cast<double*>(raw.data())[i] = values[i];
+            else
+                reinterpret_cast<float*>(raw.data())[i] = (float)values[i];
+        }
+        CK(cudaMemcpy(static_cast<char*>(g->buf[act]) + (size_t)pool * raw.size(), raw.data(),
+                      raw.size(), cudaMemcpyHostToDevice));
+    }
+    m.tracked[act] = tracked;
+    m.withheld[act] = withheld;
+    CK(cudaMemcpy(g->meta + pool, &m, sizeof(m), cudaMemcpyHostToDevice));
+    return WRNG_GPU_OK;
+}
+
+wrng_gpu_status wrng_gpu_read_uniform(wrng_gpu_t* g, uint32_t pool, uint64_t* table607,
+                                      uint32_t* cursor_r, uint32_t* cursor_s,
+                                      uint64_t* draws) {
+    if (!g || pool >= g->cfg.pools) return WRNG_GPU_EINVAL;
+    DeviceGuard dg(g->cfg.device);
+    wrng_gpu_status st = collect(g);
+    if (st) return st;
+    LfgState l;
+    CK(cudaMemcpy(&l, g->lfg + pool, sizeof(l), cudaMemcpyDeviceToHost));
+    if (table607) std::memcpy(table607, l.table, sizeof(l.table));
+    if (cursor_r) *cursor_r = l.r;
+    if (cursor_s) *cursor_s = (l.r + kGap) % kTable;
+    if (draws) *draws = l.draws;
+    return WRNG_GPU_OK;
+}
+
+wrng_gpu_status wrng_gpu_export_state(wrng_gpu_t* g, uint8_t* buf, size_t cap, size_t* size) {
+    if (!g || !size) return WRNG_GPU_EINVAL;
+    DeviceGuard dg(g->cfg.device);
+    wrng_gpu_status st = collect(g);
+    if (st) return st;
+    const uint32_t P = g->cfg.pools;
+    std::vector<PoolMeta> m(P);
+    std::vector<LfgState> l(P);
+    CK(cudaMemcpy(m.data(), g->meta, sizeof(PoolMeta) * P, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(l.data(), g->lfg, sizeof(LfgState) * P, cudaMemcpyDeviceToHost));
+    const size_t pbytes = g->nvals * g->esize;
+    std::vector<uint8_t> vals[2];
+    for (int b = 0; b < 2; ++b) {
+        vals[b].resize(pbytes * P);
+        CK(cudaMemcpy(vals[b].data(), g->buf[b], vals[b].size(), cudaMemcpyDeviceToHost));
+    }
+    const bool v1 = g->cfg.n_arrays == 2 && g->cfg.dtype == WRNG_GPU_F64 && P == 1;
+    Writer w;
+    // header (serialize.cpp:82-96)
+    w.u32(kMagic);
+    w.u32(v1 ? 1 : 2);
+    w.u32(g->cfg.pool_exponent);
+    w.u32(g->cfg.throwaway_f);
+    w.u8((uint8_t)g->cfg.scale_mode);
+    w.u64(g->cfg.restart_interval_passes);
+    w.u64(g->cfg.drift_check_period);
+    w.u64(g->cfg.seed);
+    w.u64(g->cfg.stream_id);
+    if (!v1) {
+        w.u32(g->cfg.n_arrays);
+        w.u32(g->cfg.dtype);
+        w.u32(P);
+    }
+    for (uint32_t p = 0; p < P; ++p) {
+        const Ctr& c = g->ctr[p];
+        w.u64(c.pc);
+        w.u64(c.emitted);
+        w.u64(c.avail);
+        w.u8((uint8_t)c.active);
+        for (uint32_t i = 0; i < kTable; ++i) w.u64(l[p].table[i]);  // (serialize.cpp:98-101)
+        w.u32(l[p].r);
+        w.u32((l[p].r + kGap) % kTable);
+        w.u64(l[p].draws);
+        for (int b = 0; b < 2; ++b) {  // both pools (serialize.cpp:103-110)
+            const uint8_t* src = vals[b].data() + p * pbytes;
+            if (v1) {
+                const double* d = reinterpret_cast<const double*>(src);
+                for (uint64_t i = 0; i < g->nvals; ++i) w.f64(d[i]);
+            } else {
+                w.raw(src, pbytes);  // little-endian IEEE bit patterns
+            }
+            w.f64(m[p].tracked[b]);
+            w.f64(m[p].withheld[b]);
+        }
+    }
+    *size = w.b.size();
+    if (buf && cap >= w.b.size()) std::memcpy(buf, w.b.data(), w.b.size());
+    return WRNG_GPU_OK;
+}
+
+wrng_gpu_status wrng_gpu_import_state(const uint8_t* bytes, size_t size, int32_t device,
+                                      uint32_t flags, wrng_gpu_t** out) {
+    if (!out || (!bytes && size)) return WRNG_GPU_EINVAL;
+    *out = nullptr;
+    Reader r{bytes, size};
+    // load_state (serialize.cpp:115-169): magic, version, then fields with
+    // range checks; truncation and trailing bytes are errors.
+    uint32_t magic = r.u32();
+    if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
+    if (magic != kMagic) return WRNG_GPU_EMALFORMED_BAD_MAGIC;
+    uint32_t ver = r.u32();
+    if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
+    if (ver != 1 && ver != 2) return WRNG_GPU_EMALFORMED_VERSION;
+    wrng_gpu_config c;
+    wrng_gpu_config_default(&c);
+    c.device = device;
+    c.flags = flags & ~WRNG_GPU_INIT_HOST;
+    c.pool_exponent = r.u32();
+    if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
+    if (c.pool_exponent < 8 || c.pool_exponent > 20) return WRNG_GPU_EMALFORMED_FIELD_RANGE;
+    c.throwaway_f = r.u32();
+    if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
+    if (c.throwaway_f < 1) return WRNG_GPU_EMALFORMED_FIELD_RANGE;
+    uint8_t mode = r.u8();
+    if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
+    if (mode > 1) return WRNG_GPU_EMALFORMED_FIELD_RANGE;
+    c.scale_mode = mode;
+    c.restart_interval_passes = r.u64();
+    c.drift_check_period = r.u64();
+    c.seed = r.u64();
+    c.stream_id = r.u64();
+    if (ver == 2) {
+        c.n_arrays = r.u32();
+        c.dtype = r.u32();
+        c.pools = r.u32();
+        if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
+        if ((c.n_arrays != 2 && c.n_arrays != 4) || c.dtype > 1 || c.pools < 1 ||
+            c.pools > (1u << 20))
+            return WRNG_GPU_EMALFORMED_FIELD_RANGE;
+    }
+    if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
+    const uint32_t N = 1u << c.pool_exponent;
+    const uint64_t nvals = (uint64_t)c.n_arrays * N;
+    const size_t esz = c.dtype == WRNG_GPU_F64 ? 8 : 4;
+    const uint32_t P = c.pools;
+    std::vector<Ctr> ctr(P);
+    std::vector<LfgState> lfg(P);
+    std::vector<PoolMeta> meta(P);
+    std::vector<uint8_t> vals[2];
+    vals[0].resize(nvals * esz * P);
+    vals[1].resize(nvals * esz * P);
+    for (uint32_t p = 0; p < P; ++p) {
+        ctr[p].pc = r.u64();
+        ctr[p].emitted = r.u64();
+        ctr[p].avail = r.u64();
+        if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
+        if (ctr[p].avail > nvals - 1) return WRNG_GPU_EMALFORMED_FIELD_RANGE;
+        uint8_t act = r.u8();
+        if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
+        if (act > 1) return WRNG_GPU_EMALFORMED_FIELD_RANGE;
+        ctr[p].active = act;
+        for (uint32_t i = 0; i < kTable; ++i) lfg[p].table[i] = r.u64();
+        uint32_t cr = r.u32(), cs = r.u32();
+        if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
+        if (cr >= kTable || cs >= kTable) return WRNG_GPU_EMALFORMED_FIELD_RANGE;
+        if ((cs + kTable - cr) % kTable != kGap) return WRNG_GPU_EMALFORMED_FIELD_RANGE;
+        lfg[p].r = cr;
+        lfg[p].draws = r.u64();
+        for (int b = 0; b < 2; ++b) {
+            uint8_t* dst = vals[b].data() + p * nvals * esz;
+            if (ver == 1) {
+                for (uint64_t i = 0; i < nvals; ++i) {
+                    double d = r.f64();
+                    std::memcpy(dst + i * 8, &d, 8);
+                }
+            } else {
+                r.raw(dst, nvals * esz);
+            }
+            meta[p].tracked[b] = r.f64();
+            meta[p].withheld[b] = r.f64();
+        }
+        if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
+        meta[p].pass_count = ctr[p].pc;
+        meta[p].avail = ctr[p].avail;
+        meta[p].emitted = ctr[p].emitted;
+        meta[p].active = ctr[p].active;
+        meta[p].error = 0;
+    }
+    if (r.pos != size) return WRNG_GPU_EMALFORMED_FIELD_RANGE;  // trailing bytes
+    wrng_gpu* g = nullptr;
+    wrng_gpu_status st = alloc_handle(&c, &g);
+    if (st) {
+        wrng_gpu_destroy(g);
+        return st;
+    }
+    DeviceGuard dg(device);
+    g->ctr = ctr;
+    for (int b = 0; b < 2; ++b) {
+        cudaError_t e = cudaMemcpy(g->buf[b], vals[b].data(), vals[b].size(),
+                                   cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            wrng_gpu_destroy(g);
+            return WRNG_GPU_ECUDA;
+        }
+    }
+    if (cudaMemcpy(g->lfg, lfg.data(), sizeof(LfgState) * P, cudaMemcpyHostToDevice) !=
+            cudaSuccess ||
+        cudaMemcpy(g->meta, meta.data(), sizeof(PoolMeta) * P, cudaMemcpyHostToDevice) !=
+            cudaSuccess) {
+        wrng_gpu_destroy(g);
+        return WRNG_GPU_ECUDA;
+    }
+    *out = g;
+    return WRNG_GPU_OK;
+}
+
+wrng_gpu_status wrng_gpu_synchronize(wrng_gpu_t* g) {
+    if (!g) return WRNG_GPU_EINVAL;
+    DeviceGuard dg(g->cfg.device);
+    return collect(g);
+}
+
+const char* wrng_gpu_last_error(const wrng_gpu_t* g) { return g ? g->err.c_str() : ""; }
+
+uint64_t wrng_gpu_kernel_launches(const wrng_gpu_t* g) { return g ? g->launches : 0; }
+
+const char* wrng_gpu_engine(const wrng_gpu_t* g) { return g && g->hbm ? "hbm" : "smem"; }
+
+static wrng_gpu_status moments_any(const void* dev, int is_f32, uint64_t n, double* out5,
+                                   int32_t device, void* stream) {
+    if (!dev || !out5 || n == 0) return WRNG_GPU_EINVAL;
+    DeviceGuard dg(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint32_t nb = 148 * 8;
+    double* part = nullptr;
+    if (cudaMalloc(&part, sizeof(double) * (nb * 4 + 8)) != cudaSuccess) return WRNG_GPU_ENOMEM;
+    cudaError_t e = launch_moments(dev, is_f32, n, part, nb, part + nb * 4, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(out5, part + nb * 4, sizeof(double) * 5, cudaMemcpyDeviceToHost);
+    cudaFree(part);
+    return e == cudaSuccess ? WRNG_GPU_OK : WRNG_GPU_ECUDA;
+}
+
+wrng_gpu_status wrng_gpu_moments_f32(const float* dev, uint64_t n, double* out5, int32_t device,
+                                     void* stream) {
+    return moments_any(dev, 1, n, out5, device, stream);
+}
+
+wrng_gpu_status wrng_gpu_moments_f64(const double* dev, uint64_t n, double* out5,
+                                     int32_t device, void* stream) {
+    return moments_any(dev, 0, n, out5, device, stream);
+}
+
+wrng_gpu_status wrng_gpu_lfg_words(uint64_t seed, uint64_t stream_id, uint32_t pools,
+                                   uint64_t count, uint64_t* host_out, int32_t device) {
+    if (!host_out || pools == 0) return WRNG_GPU_EINVAL;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return WRNG_GPU_ENODEV;
+    DeviceGuard dg(device);
+    uint64_t* d = nullptr;
+    const size_t bytes = sizeof(uint64_t) * count * pools;
+    if (cudaMalloc(&d, bytes ? bytes : 8) != cudaSuccess) return WRNG_GPU_ENOMEM;
+    cudaError_t e = launch_lfg_words(seed, stream_id, pools, count, d, nullptr);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess && bytes) e = cudaMemcpy(host_out, d, bytes, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? WRNG_GPU_OK : WRNG_GPU_ECUDA;
+}
+
+}  // extern "C"

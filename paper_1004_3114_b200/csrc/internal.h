@@ -1,0 +1,122 @@
+// Internal declarations shared by kernels.cu (device code + launchers) and
+// capi.cu (the extern "C" ABI in include/wrng_gpu.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "wrng_gpu.h"
+
+namespace wg {
+
+constexpr uint32_t kTable = 607;          // lag table size (uniform.hpp:17)
+constexpr uint32_t kShortLag = 273;       // (uniform.hpp:18)
+constexpr uint32_t kGap = kTable - kShortLag;  // cursor_s - cursor_r = 334
+constexpr uint32_t kWarmup = 10 * kTable;      // uniform.cpp:30
+
+// Per-pool uniform generator, device resident (UniformState, uniform.hpp:16-29).
+// cursor_s is implied: (r + 334) mod 607 (serialize.cpp:145-148 invariant).
+struct LfgState {
+    uint64_t table[kTable];
+    uint32_t r;
+    uint32_t pad_;
+    uint64_t draws;
+};
+
+// Per-pool bookkeeping, device resident.  tracked/withheld per buffer as in
+// Pool (wallace.hpp:36-40); counters as in WallaceState (wallace.hpp:167-172).
+struct PoolMeta {
+    double tracked[2];
+    double withheld[2];
+    uint64_t pass_count;
+    uint64_t avail;
+    uint64_t emitted;
+    uint32_t active;
+    uint32_t error;  // 0, or a wrng_gpu_status raised on the device
+};
+
+enum Op : uint32_t {
+    OP_FILL = 0,     // WallaceState::fill
+    OP_PASSES = 1,   // advance_pass x npasses
+    OP_REFILL = 2,   // refill
+    OP_DRIFT = 3,    // drift_check
+    OP_RESTART = 4,  // restart
+    OP_INIT = 5,     // seed uniform generators + init_pool
+};
+
+// Output placement of a bank fill: pool p writes len_p values at
+// out + p * off_stride + min(p, off_extra), len_p = len_base + (p < len_extra).
+struct OutLayout {
+    uint64_t off_stride;
+    uint64_t off_extra;
+    uint64_t len_base;
+    uint64_t len_extra;
+};
+
+struct KernelArgs {
+    void* buf[2];          // pool double buffer, pools * n_arrays * N each
+    PoolMeta* meta;        // [pools]
+    LfgState* lfg;         // [pools]
+    void* out;             // output (device)
+    OutLayout lay;
+    double mu, sigma;
+    uint32_t out_f32;      // 1: float output, 0: double output
+    uint32_t unit;         // mu == 0 && sigma == 1
+    uint32_t N;            // per-array length
+    uint32_t f;            // throwaway_f
+    uint32_t mode;         // scale mode
+    uint32_t op;           // Op
+    uint32_t npasses;      // OP_PASSES
+    uint32_t pools;
+    uint64_t restart;      // restart_interval_passes
+    uint64_t drift;        // drift_check_period
+    uint64_t seed, stream0;  // OP_INIT
+    wrng_gpu_params* params_out;  // OP_PASSES: [pools], params of the last pass
+};
+
+struct EngineShape {
+    uint32_t threads;   // CTA size
+    uint32_t smem;      // dynamic shared memory bytes
+    uint32_t j;         // pool columns per thread
+};
+
+// Shared-memory engine: one CTA per pool.
+bool smem_engine_fits(uint32_t n_arrays, uint32_t dtype, uint32_t N);
+EngineShape smem_engine_shape(uint32_t n_arrays, uint32_t dtype, uint32_t N);
+cudaError_t launch_smem(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
+                        cudaStream_t st);
+
+// HBM engine: one grid-wide launch per pass.
+struct HbmPass {
+    uint32_t src;        // buffer index read
+    uint32_t param_idx;  // index into the per-pool params array
+    uint64_t emit_n;     // emit flat [0, emit_n) of the new pool
+    uint64_t out_off;    // ... to out + out_off
+    uint32_t end_refill; // 1: last pass of a refill (sets avail = cap - emit_n)
+};
+cudaError_t launch_hbm_params(uint32_t n_arrays, uint32_t N, LfgState* lfg,
+                              wrng_gpu_params* params, uint32_t npass, PoolMeta* meta,
+                              cudaStream_t st);
+cudaError_t launch_hbm_pass(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
+                            wrng_gpu_params* params, const HbmPass& ps,
+                            cudaStream_t st);
+cudaError_t launch_hbm_emit(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
+                            uint32_t buf, uint64_t pos, uint64_t take, uint64_t out_off,
+                            cudaStream_t st);
+cudaError_t launch_hbm_drift(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
+                             uint32_t buf, int tree, double* scratch,
+                             cudaStream_t st);
+cudaError_t launch_hbm_init(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
+                            uint32_t buf, int seed_lfg, cudaStream_t st);
+cudaError_t launch_hbm_setmeta(PoolMeta* meta, uint64_t pass_count, uint64_t avail,
+                               uint64_t emitted, uint32_t active, cudaStream_t st);
+
+// Validation reductions.
+cudaError_t launch_moments(const void* v, int is_f32, uint64_t n, double* partials,
+                           uint32_t nblocks, double* out5_dev, cudaStream_t st);
+
+// Device uniform generator words (tests).
+cudaError_t launch_lfg_words(uint64_t seed, uint64_t stream0, uint32_t pools,
+                             uint64_t count, uint64_t* out, cudaStream_t st);
+
+}  // namespace wg

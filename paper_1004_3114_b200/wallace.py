@@ -1,0 +1,367 @@
+"""Python mirror of the reference generator interface over the GPU C ABI.
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/include/wrng/wallace.hpp (WallaceConfig, ScaleMode,
+PassParams, Pool, WallaceState) and errors.hpp (corrupted_state_error,
+malformed_state_error{kind}); std::invalid_argument maps to ValueError.  The
+C++ mirror for C++ callers is include/wrng_gpu/wallace.hpp.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional, Union
+
+import numpy as np
+
+from . import _lib as L
+
+lib = L.lib
+
+
+class ScaleMode(enum.IntEnum):  # wallace.hpp:52-55
+    chisq = 0
+    fixed = 1
+
+
+class StateErrorKind(enum.IntEnum):  # errors.hpp:15-20
+    bad_magic = 0
+    unsupported_version = 1
+    truncated = 2
+    field_range = 3
+
+
+class CorruptedStateError(RuntimeError):
+    """wrng::corrupted_state_error (errors.hpp:10-13)."""
+
+
+class MalformedStateError(RuntimeError):
+    """wrng::malformed_state_error (errors.hpp:22-32)."""
+
+    def __init__(self, kind: StateErrorKind, what: str):
+        super().__init__(what)
+        self.kind = kind
+
+
+class CudaError(RuntimeError):
+    """Device-side failure (no reference analogue)."""
+
+
+_MALFORMED = {
+    L.EMALFORMED_BAD_MAGIC: StateErrorKind.bad_magic,
+    L.EMALFORMED_VERSION: StateErrorKind.unsupported_version,
+    L.EMALFORMED_TRUNCATED: StateErrorKind.truncated,
+    L.EMALFORMED_FIELD_RANGE: StateErrorKind.field_range,
+}
+
+
+def _raise(rc: int, what: str, h=None):
+    if rc == L.OK:
+        return
+    msg = what
+    if h is not None:
+        detail = lib.wrng_gpu_last_error(h)
+        if detail:
+            msg = f"{what}: {detail.decode()}"
+    if rc == L.EINVAL:
+        raise ValueError(msg)
+    if rc == L.ECORRUPT:
+        raise CorruptedStateError(msg)
+    if rc in _MALFORMED:
+        raise MalformedStateError(_MALFORMED[rc], msg)
+    raise CudaError(f"{msg} (status {rc})")
+
+
+@dataclass
+class WallaceConfig:
+    """wallace.hpp:57-65, plus the B200 extensions (n_arrays, dtype, pools, ...)."""
+
+    pool_exponent: int = 10
+    throwaway_f: int = 3
+    scale_mode: ScaleMode = ScaleMode.chisq
+    restart_interval_passes: int = 0
+    drift_check_period: int = 64
+    seed: int = 0
+    stream_id: int = 0
+    # extensions
+    n_arrays: int = 2          # 2 (reference) or 4 (docs/n4_spec.md)
+    dtype: str = "f64"         # "f64" | "f32"
+    pools: int = 1             # independent pools, pool p = stream_id + p
+    device: int = 0
+    init_on_host: bool = False  # glibc Box-Muller init (bit-exact with the reference)
+    force_hbm: bool = False     # HBM-resident engine even when smem would fit
+    drift_tree: bool = False    # parallel (non-reference-order) drift sum
+
+    def to_c(self) -> L.Config:
+        c = L.Config()
+        lib.wrng_gpu_config_default(C.byref(c))
+        c.pool_exponent = self.pool_exponent
+        c.throwaway_f = self.throwaway_f
+        c.scale_mode = int(self.scale_mode)
+        c.restart_interval_passes = self.restart_interval_passes
+        c.drift_check_period = self.drift_check_period
+        c.seed = self.seed & (2**64 - 1)
+        c.stream_id = self.stream_id & (2**64 - 1)
+        c.n_arrays = self.n_arrays
+        c.dtype = L.F64 if self.dtype == "f64" else L.F32
+        c.pools = self.pools
+        c.device = self.device
+        c.flags = ((L.FLAG_INIT_HOST if self.init_on_host else 0)
+                   | (L.FLAG_FORCE_HBM if self.force_hbm else 0)
+                   | (L.FLAG_DRIFT_TREE if self.drift_tree else 0))
+        return c
+
+    @classmethod
+    def from_c(cls, c: L.Config) -> "WallaceConfig":
+        return cls(pool_exponent=c.pool_exponent, throwaway_f=c.throwaway_f,
+                   scale_mode=ScaleMode(c.scale_mode),
+                   restart_interval_passes=c.restart_interval_passes,
+                   drift_check_period=c.drift_check_period, seed=c.seed,
+                   stream_id=c.stream_id, n_arrays=c.n_arrays,
+                   dtype="f64" if c.dtype == L.F64 else "f32", pools=c.pools,
+                   device=c.device, init_on_host=bool(c.flags & L.FLAG_INIT_HOST),
+                   force_hbm=bool(c.flags & L.FLAG_FORCE_HBM),
+                   drift_tree=bool(c.flags & L.FLAG_DRIFT_TREE))
+
+
+@dataclass
+class Rotation2:  # wallace.hpp:14-17
+    c: float
+    s: float
+
+
+@dataclass
+class PassParams:
+    """wallace.hpp:22-30; n = 4 adds strides[2:], offsets[2:] and `variant`."""
+
+    alpha: int
+    beta: int
+    gamma: int
+    delta: int
+    rot: Rotation2
+    scale: float
+    target_sumsq: float
+    strides: List[int] = field(default_factory=list)
+    offsets: List[int] = field(default_factory=list)
+    variant: int = 0
+
+    @classmethod
+    def from_c(cls, p: L.Params, n_arrays: int) -> "PassParams":
+        return cls(alpha=p.stride[0], beta=p.stride[1], gamma=p.offset[0], delta=p.offset[1],
+                   rot=Rotation2(p.c, p.s), scale=p.scale, target_sumsq=p.target_sumsq,
+                   strides=list(p.stride)[:n_arrays], offsets=list(p.offset)[:n_arrays],
+                   variant=p.variant)
+
+
+@dataclass
+class Pool:
+    """wallace.hpp:36-50: the live pool as host arrays (arrays[m] is x_m)."""
+
+    arrays: np.ndarray  # (n_arrays, N) float64
+    tracked_sumsq: float
+    withheld: float
+
+    @property
+    def x(self) -> np.ndarray:
+        return self.arrays[0]
+
+    @property
+    def y(self) -> np.ndarray:
+        return self.arrays[1]
+
+    def n(self) -> int:
+        return self.arrays.shape[1]
+
+    def direct_sumsq(self) -> float:
+        """Sequential sum, arrays in order (wallace.hpp:44-46)."""
+        q = 0.0
+        for v in self.arrays.reshape(-1).tolist():
+            q += v * v
+        return q
+
+    def max_abs(self) -> float:
+        return float(np.max(np.abs(self.arrays)))
+
+
+@dataclass
+class UniformStateView:
+    """uniform.hpp:16-29 snapshot."""
+
+    lag_table: np.ndarray
+    cursor_r: int
+    cursor_s: int
+    draws: int
+
+
+def _is_device_tensor(t) -> bool:
+    return hasattr(t, "data_ptr") and getattr(t, "is_cuda", False)
+
+
+class WallaceState:
+    """wallace.hpp:113-174 on the B200.  One handle may hold `pools`
+    independent generators; every call applies to all of them, and fill
+    writes pool p's stream into the p-th contiguous segment."""
+
+    def __init__(self, config: Optional[WallaceConfig] = None, *, _handle=None):
+        if _handle is not None:
+            self._h = _handle
+            c = L.Config()
+            _raise(lib.wrng_gpu_get_config(self._h, C.byref(c)), "get_config")
+            self._cfg = WallaceConfig.from_c(c)
+            return
+        self._cfg = config or WallaceConfig()
+        c = self._cfg.to_c()
+        h = C.c_void_p()
+        _raise(lib.wrng_gpu_create(C.byref(c), C.byref(h)), "WallaceState")
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.wrng_gpu_destroy(h)
+            self._h = None
+
+    # ---- generation -------------------------------------------------------
+    def fill(self, out: Union[int, np.ndarray, "object"], mu: float = 0.0,
+             sigma: float = 1.0, *, dtype: Optional[str] = None, stream=None):
+        """fill(count) -> numpy array (host output, synchronous);
+        fill(ndarray) fills a host array in place;
+        fill(torch CUDA tensor) fills device memory in place, enqueued on
+        `stream` (default: torch's current stream) without a host sync."""
+        if isinstance(out, (int, np.integer)):
+            dt = dtype or self._cfg.dtype
+            arr = np.empty(int(out), dtype=np.float64 if dt == "f64" else np.float32)
+            self.fill(arr, mu, sigma)
+            return arr
+        if isinstance(out, np.ndarray):
+            if not out.flags.c_contiguous or out.dtype not in (np.float32, np.float64):
+                raise ValueError("fill: contiguous float32/float64 array required")
+            fn = lib.wrng_gpu_fill_f64 if out.dtype == np.float64 else lib.wrng_gpu_fill_f32
+            _raise(fn(self._h, out.ctypes.data if out.size else None, out.size, mu, sigma, 0,
+                      None), "fill", self._h)
+            return out
+        if _is_device_tensor(out):
+            import torch
+
+            if not out.is_contiguous() or out.dtype not in (torch.float32, torch.float64):
+                raise ValueError("fill: contiguous float32/float64 CUDA tensor required")
+            if stream is None:
+                stream = torch.cuda.current_stream(out.device)
+            sptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+            fn = lib.wrng_gpu_fill_f64 if out.dtype == torch.float64 else lib.wrng_gpu_fill_f32
+            _raise(fn(self._h, out.data_ptr() if out.numel() else None, out.numel(), mu, sigma,
+                      1, sptr), "fill", self._h)
+            return out
+        raise TypeError("fill: expected a count, a numpy array or a CUDA tensor")
+
+    def advance_pass(self):
+        P = self._cfg.pools
+        arr = (L.Params * P)()
+        _raise(lib.wrng_gpu_advance_pass(self._h, arr), "advance_pass", self._h)
+        out = [PassParams.from_c(arr[p], self._cfg.n_arrays) for p in range(P)]
+        return out[0] if P == 1 else out
+
+    def refill(self):
+        _raise(lib.wrng_gpu_refill(self._h), "refill", self._h)
+
+    def drift_check(self):
+        _raise(lib.wrng_gpu_drift_check(self._h), "drift_check", self._h)
+
+    def restart(self):
+        _raise(lib.wrng_gpu_restart(self._h), "restart", self._h)
+
+    def synchronize(self):
+        _raise(lib.wrng_gpu_synchronize(self._h), "synchronize", self._h)
+
+    # ---- persistence (serialize.cpp:82-169) -----------------------------------
+    def save_state(self) -> bytes:
+        n = C.c_size_t()
+        _raise(lib.wrng_gpu_export_state(self._h, None, 0, C.byref(n)), "save_state", self._h)
+        buf = (C.c_uint8 * n.value)()
+        _raise(lib.wrng_gpu_export_state(self._h, buf, n.value, C.byref(n)), "save_state",
+               self._h)
+        return bytes(buf)
+
+    @classmethod
+    def load_state(cls, data: bytes, device: int = 0, *, force_hbm: bool = False,
+                   drift_tree: bool = False) -> "WallaceState":
+        h = C.c_void_p()
+        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
+        flags = (L.FLAG_FORCE_HBM if force_hbm else 0) | (L.FLAG_DRIFT_TREE if drift_tree else 0)
+        _raise(lib.wrng_gpu_import_state(buf, len(data), device, flags, C.byref(h)),
+               "load_state")
+        return cls(_handle=h)
+
+    # ---- accessors (wallace.hpp:148-160) -----------------------------------
+    @property
+    def config(self) -> WallaceConfig:
+        return self._cfg
+
+    def _counters(self, pool: int = 0) -> L.Counters:
+        c = L.Counters()
+        _raise(lib.wrng_gpu_get_counters(self._h, pool, C.byref(c)), "counters")
+        return c
+
+    def pool_size(self) -> int:
+        return 1 << self._cfg.pool_exponent
+
+    def pass_count(self, pool: int = 0) -> int:
+        return self._counters(pool).pass_count
+
+    def numbers_emitted(self, pool: int = 0) -> int:
+        return self._counters(pool).numbers_emitted
+
+    def avail(self, pool: int = 0) -> int:
+        return self._counters(pool).avail
+
+    def active_pool(self, pool: int = 0) -> Pool:
+        n = self._cfg.n_arrays * self.pool_size()
+        v = np.empty(n, dtype=np.float64)
+        t, w = C.c_double(), C.c_double()
+        _raise(lib.wrng_gpu_read_pool(self._h, pool, v.ctypes.data, C.byref(t), C.byref(w)),
+               "active_pool", self._h)
+        return Pool(v.reshape(self._cfg.n_arrays, -1), t.value, w.value)
+
+    def set_active_pool(self, p: Pool, pool: int = 0):
+        v = np.ascontiguousarray(p.arrays, dtype=np.float64).reshape(-1)
+        _raise(lib.wrng_gpu_write_pool(self._h, pool, v.ctypes.data, p.tracked_sumsq,
+                                       p.withheld), "set_active_pool", self._h)
+
+    def uniform_state(self, pool: int = 0) -> UniformStateView:
+        t = np.empty(607, dtype=np.uint64)
+        r, s, d = C.c_uint32(), C.c_uint32(), C.c_uint64()
+        _raise(lib.wrng_gpu_read_uniform(self._h, pool, t.ctypes.data, C.byref(r), C.byref(s),
+                                         C.byref(d)), "uniform_state", self._h)
+        return UniformStateView(t, r.value, s.value, d.value)
+
+    def kernel_launches(self) -> int:
+        return int(lib.wrng_gpu_kernel_launches(self._h))
+
+    def engine(self) -> str:
+        return lib.wrng_gpu_engine(self._h).decode()
+
+    @property
+    def handle(self):
+        return self._h
+
+
+def device_moments(t, device: int = 0, stream=None) -> dict:
+    """n, m1..m4 of a CUDA tensor by the device reduction (validation only)."""
+    import torch
+
+    out = np.zeros(5, dtype=np.float64)
+    if stream is None:
+        stream = torch.cuda.current_stream(t.device)
+    fn = lib.wrng_gpu_moments_f32 if t.dtype == torch.float32 else lib.wrng_gpu_moments_f64
+    _raise(fn(t.data_ptr(), t.numel(), out.ctypes.data, device, stream.cuda_stream),
+           "moments")
+    return {"n": int(out[0]), "m1": out[1], "m2": out[2], "m3": out[3], "m4": out[4]}
+
+
+def lfg_words(seed: int, stream_id: int, pools: int, count: int, device: int = 0) -> np.ndarray:
+    """First `count` next_word() outputs of UniformState(seed, stream_id + p)."""
+    out = np.empty((pools, count), dtype=np.uint64)
+    _raise(lib.wrng_gpu_lfg_words(seed, stream_id, pools, count, out.ctypes.data, device),
+           "lfg_words")
+    return out
