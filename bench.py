@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""Benchmark of the Wallace pool-regeneration hot path (BASELINE.json).
+
+Default workload:
+  N = 1 GPU : C3 — n = 4, fp32, 4 x 1024 floats per pool in shared memory,
+              8 pools per SM x 148 SMs = 1184 pools, pool c seeded
+              UniformState(2024, c), 1 pass per output, 2^34 normals per step
+              written as one contiguous fp32 array (pool-major segments).
+  N > 1     : C4 — the same pools, GPU g seeded UniformState(99 + g, c),
+              2^36 normals per step split evenly over the GPUs (strong
+              scaling), no inter-GPU communication on the generation path.
+Other configs (--config c1 | c2 | c4) print the same JSON line for those
+workloads.
+
+One "step" = one fill of the whole step's normals through the C ABI
+(wrng_gpu_fill_f32/_f64, device output).  `value` is device-timed whole-job
+normals/s (CUDA events on the launch stream, max over ranks).  `e2e` is the
+same metric through the same public call with a pinned HOST output buffer
+(generation overlapped with D2H inside the library), on a bounded sample.
+
+`--impl reference` times the reference's own CPU implementation (the
+unmodified library built from /root/reference into oracle/_ref) on all host
+cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "N(0,1) normals/sec per GPU and whole box; % of HBM-store roofline"
+UNIT = "normals/s"
+SMS = 148
+
+CONFIGS = {
+    # name: (n_arrays, dtype, pool_exponent, throwaway_f, pools, seed, total normals)
+    "c1": dict(n_arrays=4, dtype="f64", pool_exponent=12, throwaway_f=1, pools=1,
+               seed=12345, total=1 << 24, desc="C1 fp64 n=4 4x4096 pool, seed 12345, f=1"),
+    "c2": dict(n_arrays=4, dtype="f64", pool_exponent=20, throwaway_f=2, pools=1, seed=7,
+               total=1 << 30, desc="C2 fp64 n=4 one HBM-resident 4x2^20 pool, seed 7, f=2"),
+    "c3": dict(n_arrays=4, dtype="f32", pool_exponent=10, throwaway_f=1, pools=8 * SMS,
+               seed=2024, total=1 << 34,
+               desc="C3 fp32 n=4 4x1024 smem pool per CTA, 8 CTAs/SM x 148, seed 2024, f=1"),
+    "c4": dict(n_arrays=4, dtype="f32", pool_exponent=10, throwaway_f=1, pools=8 * SMS,
+               seed=99, total=1 << 36,
+               desc="C4 fp32 n=4 per-CTA pools, GPU g seeded 99+g, 2^36 total split evenly"),
+}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's own CPU implementation on all host cores
+# ---------------------------------------------------------------------------
+def run_reference(args, cfgname: str, world: int, rank: int):
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    c = CONFIGS[cfgname]
+    threads = cpu_threads()
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/libwrng_ref.so not built"}))
+        return 0
+    # The reference implements n = 2 fp64 only: time it at
+    # the workload's pool size and pass count, thread t = stream t.
+    per_thread = int(args.ref_sample_per_thread)
+    p, f = c["pool_exponent"], c["throwaway_f"]
+    seed = c["seed"]
+    for _ in range(args.warmup):
+        O.ref_bench_threads(p, f, 0, seed, 0, threads, max(per_thread // 8, 1 << 16))
+    times = []
+    for _ in range(args.steps):
+        times.append(O.ref_bench_threads(p, f, 0, seed, 0, threads, per_thread))
+    total = per_thread * threads
+    ms = 1e3 * statistics.mean(times)
+    value = total / (ms / 1e3)
+    sample = (f"reference WallaceState n=2 fp64 (the only mode it implements), "
+              f"N=2^{p}, f={f}, chisq, seed {seed}, {threads} threads x {per_thread} values "
+              f"per step via fill(64Ki) (proj/tools/main.cpp:287-312 loop)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator state)",
+        "config": {"workload": c["desc"], "reference_mode": "n=2 fp64", "pool_exponent": p,
+                   "throwaway_f": f, "host_threads": threads},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def cpu_baseline_port(c, seconds_target: float):
+    """The oracle restatement (n = 4 / fp32, same workload semantics) on all
+    host cores, bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ctypes as C
+
+    import oracle as O
+
+    threads = cpu_threads()
+    cfg = O.OrConfig(c["n_arrays"], O.F64 if c["dtype"] == "f64" else O.F32, c["pool_exponent"],
+                     c["throwaway_f"], O.CHISQ, 0, 64, c["seed"], 0)
+    lib = O.oracle_lib()
+    # calibrate: 2^20 values per thread
+    probe = 1 << 20
+    t = lib.or_bench_threads(C.byref(cfg), threads, probe, 1 << 16)
+    per_thread = int(min(1 << 30, max(probe, probe * seconds_target / max(t, 1e-6))))
+    t = lib.or_bench_threads(C.byref(cfg), threads, per_thread, 1 << 16)
+    value = per_thread * threads / t
+    return {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": (f"oracle/wallace_oracle.c (n={c['n_arrays']} {c['dtype']} restatement, "
+                       f"not reference code), N=2^{c['pool_exponent']}, f={c['throwaway_f']}, "
+                       f"{threads} threads x {per_thread} values, pools = streams 0..{threads - 1}, "
+                       f"{t:.2f} s wall")}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
+    ap.add_argument("--total", type=int, default=None, help="override normals per step")
+    ap.add_argument("--e2e-sample", type=int, default=1 << 30)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=2.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-sample-per-thread", type=float, default=float(1 << 26))
+    args = ap.parse_args()
+
+    world, rank, local = dist_setup()
+    cfgname = args.config or ("c3" if world == 1 else "c4")
+    if args.impl == "reference":
+        return run_reference(args, cfgname, world, rank)
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_1004_3114_b200 import WallaceConfig, WallaceState
+
+    c = dict(CONFIGS[cfgname])
+    total = args.total or c["total"]
+    if cfgname == "c4":
+        seed = c["seed"] + rank
+        per_gpu = total // world
+    else:
+        seed = c["seed"] if world == 1 else c["seed"] + rank
+        per_gpu = total if world == 1 else total  # weak scaling for c1..c3 at N > 1
+    scaling = "strong" if cfgname == "c4" else "weak"
+    out_dtype = torch.float32 if c["dtype"] == "f32" else torch.float64
+    esize = 4 if c["dtype"] == "f32" else 8
+
+    gen = WallaceState(WallaceConfig(pool_exponent=c["pool_exponent"],
+                                     throwaway_f=c["throwaway_f"], seed=seed, stream_id=0,
+                                     n_arrays=c["n_arrays"], dtype=c["dtype"], pools=c["pools"],
+                                     device=local))
+    # Output buffer: the whole step when it fits in HBM, else slabs of <= 64 GiB
+    # re-used within the step (every value is still stored to HBM).
+    free, _ = torch.cuda.mem_get_info(dev)
+    slab = per_gpu
+    while slab * esize > min(free - (8 << 30), 96 << 30):
+        slab = (slab + 1) // 2
+    nslabs = math.ceil(per_gpu / slab)
+    out = torch.empty(slab, dtype=out_dtype, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        left = per_gpu
+        while left > 0:
+            n = min(slab, left)
+            gen.fill(out[:n], stream=stream)
+            left -= n
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    gen.synchronize()
+
+    # ---- timed region -----------------------------------------------------
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = gen.kernel_launches()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev[0].record(stream)
+    for k in range(args.steps):
+        step()
+        ev[k + 1].record(stream)
+    torch.cuda.synchronize(dev)
+    launches = gen.kernel_launches() - launches0
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    gen.synchronize()  # surfaces any device-raised error
+    step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    elapsed_ms = ev[0].elapsed_time(ev[-1])
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    total_normals = per_gpu * world
+    value = total_normals / (ms_per_step / 1e3)
+
+    # Roofline of the dominant kernel: one fill kernel per slab (smem engine),
+    # algorithmic bytes = stored output bytes.
+    peak, peak_src = peaks()
+    if gen.engine() == "smem":
+        launches_per_step = nslabs
+        kernel_ms = statistics.mean(step_ms) / launches_per_step
+        algo_bytes = per_gpu * esize / launches_per_step
+    else:
+        kernel_ms = statistics.mean(step_ms)
+        algo_bytes = per_gpu * esize
+    achieved = algo_bytes / (kernel_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as fh:
+                tj = json.load(fh)
+            if cfgname in tj:
+                traffic = tj[cfg_name_key(cfgname)]["bytes_per_output_byte"] * algo_bytes
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": algo_bytes,
+                "kernel_ms": kernel_ms}
+
+    # ---- e2e: same public call, HOST output (pinned), bounded sample -------
+    e2e = None
+    if rank == 0 or True:
+        n_e2e = min(args.e2e_sample, per_gpu)
+        host = torch.empty(n_e2e, dtype=out_dtype, pin_memory=True)
+        hv = host.numpy()
+        gen.fill(hv)  # warm (allocates staging)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            gen.fill(hv)
+        t1 = time.perf_counter()
+        e2e_local = n_e2e * args.e2e_steps / (t1 - t0)
+        if world > 1:
+            t = torch.tensor([t1 - t0], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_local = n_e2e * args.e2e_steps * world / float(t.item())
+        e2e = {"value": e2e_local, "unit": UNIT, "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": n_e2e * esize,
+               "sample": f"{n_e2e} normals per rank per step into pinned host memory via "
+                         f"wrng_gpu_fill_{c['dtype']}(out_is_device=0); generator state is "
+                         f"device-resident, so no host->device input bytes"}
+        del host
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None, "dtype": c["dtype"],
+        "data": "synthetic (seeded generator pools; no dataset)",
+        "config": {"workload": c["desc"], "normals_per_step": total_normals,
+                   "normals_per_gpu": per_gpu, "pools_per_gpu": c["pools"],
+                   "n_arrays": c["n_arrays"], "pool_exponent": c["pool_exponent"],
+                   "throwaway_f": c["throwaway_f"], "seed_base": c["seed"],
+                   "engine": gen.engine(), "output_slabs_per_step": nslabs,
+                   "l2": "output per step >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"independent pools, {world} GPU(s), no collective"},
+        "per_gpu_value": value / world,
+        "roofline": roofline,
+        "gpu_launches": launches,
+        "clocks": clk,
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_port(c, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def cfg_name_key(name: str) -> str:
+    return name
+
+
+if __name__ == "__main__":
+    sys.exit(main())

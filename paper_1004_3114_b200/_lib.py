@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libwrng_gpu.so")
+LIB_PATH = os.environ.get("WRNG_GPU_LIB") or os.path.join(HERE, "libwrng_gpu.so")
 
 # wrng_gpu_status
 OK = 0

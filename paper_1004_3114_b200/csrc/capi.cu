@@ -433,12 +433,15 @@ wrng_gpu_status do_fill(wrng_gpu* g, void* out, int out_f32, uint64_t count, dou
     if (sigma < 0.0) return fail(g, WRNG_GPU_EINVAL, "fill: sigma must be >= 0");
     if (count > 0 && !out) return fail(g, WRNG_GPU_EINVAL, "fill: null output");
     DeviceGuard dg(g->cfg.device);
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
     if (count == 0) {
         for (auto& c : g->ctr) plan_fill(g, c, 0, nullptr);
         return WRNG_GPU_OK;
     }
-    if (!out_is_device) return fill_host(g, out, out_f32, count, mu, sigma, s);
+    if (!out_is_device)
+        return fill_host(g, out, out_f32, count, mu, sigma,
+                         stream ? static_cast<cudaStream_t>(stream) : g->stream);
+    // Device output: the caller's stream; NULL is the legacy default stream.
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
     const uint32_t P = g->cfg.pools;
     OutLayout lay{count / P, count % P, count / P, count % P};
     return fill_device(g, out, out_f32, lay, mu, sigma, s);
@@ -637,6 +640,7 @@ wrng_gpu_status alloc_handle(const wrng_gpu_config* cfg, wrng_gpu** out) {
     CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&g->order_ev, cudaEventDisableTiming));
+    smem_engine_probe(g->stream);
     return WRNG_GPU_OK;
 }
 

@@ -1,0 +1,326 @@
+// Device helpers shared by the engines: bit-exact scalar restatements of the
+// reference, the CTA-cooperative lagged-Fibonacci generator and the device
+// Box-Muller initialisation.
+//
+// Reference (paths relative to /root/reference/proj):
+//   uniform generator      src/uniform.cpp:13-51
+//   Box-Muller             src/reference.cpp:9-22, 41-58
+//   pass parameters        src/wallace.cpp:27-70
+//   init_pool              src/wallace.cpp:158-167
+//
+// Compiled with -fmad=false: every floating-point expression is evaluated
+// exactly as written (one rounding per operation), matching the reference's
+// FMA-free Release build.  sqrt and / are IEEE-rounded on
+// the device; log/cos/sin appear only in the device Box-Muller path.
+#pragma once
+
+#include "internal.h"
+
+namespace wg {
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) {
+    return a < b ? a : b;
+}
+
+__device__ __forceinline__ double u53(uint64_t w) {
+    // next_uniform (uniform.cpp:42-45): top 53 bits * 2^-53
+    return (double)(w >> 11) * 0x1.0p-53;
+}
+__device__ __forceinline__ uint32_t nib(uint64_t w, uint32_t m) {
+    // next_int_below (uniform.cpp:47-51)
+    return (uint32_t)(u53(w) * (double)m);
+}
+__device__ __forceinline__ double chi2_target(double r, uint32_t nu) {
+    // wallace.cpp:27-31
+    double t = r + sqrt(2.0 * (double)nu - 1.0);
+    return 0.5 * t * t;
+}
+__device__ __forceinline__ uint64_t splitmix64_at(uint64_t x) {
+    // uniform.cpp:13-19 in counter form: output i = mix(s0 + (i + 1) * golden)
+    uint64_t z = x;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ bool crossed(uint64_t before, uint64_t after, uint64_t period) {
+    // wallace.cpp:182-184
+    return period > 0 && after / period > before / period;
+}
+
+// Uniform words consumed by one pass: n = 2: alpha, beta, gamma, delta, u,
+// region (wallace.cpp:54-58, 44-49); n = 4: 4 strides, 4 offsets, variant
+// (docs/n4_spec.md §2).
+template <int NA>
+struct PassWords {
+    static constexpr int K = NA == 2 ? 6 : 9;
+};
+
+// The uniform-generator part of a pass's parameters.
+struct LfgParams {
+    uint32_t stride[4];
+    uint32_t offset[4];
+    uint32_t variant;
+    uint32_t pad_;
+    double c, s;  // n = 2 rotation
+};
+
+template <int NA>
+__device__ __forceinline__ void lfg_params(const uint64_t* w, uint32_t N, LfgParams& p) {
+    if (NA == 2) {
+        p.stride[0] = nib(w[0], 2) == 0 ? 3 : 5;
+        p.stride[1] = nib(w[1], 2) == 0 ? 7 : 11;
+        p.stride[2] = p.stride[3] = 0;
+        p.offset[0] = nib(w[2], N);
+        p.offset[1] = nib(w[3], N);
+        p.offset[2] = p.offset[3] = 0;
+        p.variant = 0;
+        // rotation_from_uniform / rotation_from_t (wallace.cpp:33-49)
+        const double kTanLo = 0x1.126145e9ecd56p-2;    // 0.26794919243112270
+        const double kTanSpan = 0x1.3cd3a2c8198e2p-2;  // kTanHi - kTanLo, rounded
+        double t = kTanLo + kTanSpan * u53(w[4]);
+        uint32_t region = nib(w[5], 3);
+        double t2 = t * t;
+        double c = (1.0 - t2) / (1.0 + t2);
+        double s = 2.0 * t / (1.0 + t2);
+        if (region == 0) {
+            p.c = c;
+            p.s = s;
+        } else if (region == 1) {
+            p.c = c;
+            p.s = -s;
+        } else {
+            p.c = -c;
+            p.s = s;
+        }
+    } else {
+        // strides from {3,5}, {7,11}, {13,17}, {19,23} (docs/n4_spec.md §2)
+        const uint32_t lo[4] = {3, 7, 13, 19}, hi[4] = {5, 11, 17, 23};
+#pragma unroll
+        for (int m = 0; m < 4; ++m) p.stride[m] = nib(w[m], 2) == 0 ? lo[m] : hi[m];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) p.offset[m] = nib(w[4 + m], N);
+        p.variant = nib(w[8], 2);
+        p.c = 0.0;
+        p.s = 0.0;
+    }
+    p.pad_ = 0;
+}
+
+// Scale part of select_pass_params (wallace.cpp:59-69): 0 or ECORRUPT.
+__device__ __forceinline__ int pass_scale(double tracked, double withheld, uint32_t nu,
+                                          uint32_t mode, double& scale, double& target) {
+    if (!(tracked > 0.0)) return WRNG_GPU_ECORRUPT;
+    if (mode == WRNG_GPU_CHISQ) {
+        target = chi2_target(withheld, nu);
+        scale = sqrt(target / tracked);
+    } else {
+        scale = 1.0;
+        target = tracked;
+    }
+    return 0;
+}
+
+// Box-Muller pair (reference.cpp:9-22), u1 == 0 mapped to 2^-53.
+__device__ __forceinline__ void box_muller(uint64_t w1, uint64_t w2, double& x, double& y) {
+    double u1 = u53(w1);
+    if (u1 == 0.0) u1 = 0x1.0p-53;
+    double u2 = u53(w2);
+    const double pi = 0x1.921fb54442d18p+1;
+    double radius = sqrt(-2.0 * log(u1));
+    double angle = 2.0 * pi * u2;
+    x = radius * cos(angle);
+    y = radius * sin(angle);
+}
+
+// Output element mu + sigma * v (wallace.cpp:209-212) in double, narrowed
+// for f32 outputs; `unit` (mu = 0, sigma = 1) keeps the reference's
+// -0.0 -> +0.0 of `0 + 1 * v` without the double multiply.
+template <typename T>
+__device__ __forceinline__ void put_out(void* out, uint64_t i, T v, uint32_t out_f32,
+                                        uint32_t unit, double mu, double sigma) {
+    if (unit) {
+        if (out_f32)
+            static_cast<float*>(out)[i] = (float)v + 0.0f;
+        else
+            static_cast<double*>(out)[i] = (double)v + 0.0;
+    } else {
+        double o = mu + sigma * (double)v;
+        if (out_f32)
+            static_cast<float*>(out)[i] = (float)o;
+        else
+            static_cast<double*>(out)[i] = o;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-cooperative uniform generator.
+//
+// x_n = x_{n-607} + x_{n-273} (mod 2^64).  With the table as a 607-word ring
+// and cursor r, word k of a step (k < 273) reads slots r+k and r+k+334 and
+// writes slot r+k: no slot written in a step is read by another thread of
+// the same step, so up to 256 consecutive words are produced in parallel.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t lfg_word_at(uint64_t* tab, uint32_t r, uint32_t k) {
+    uint32_t i = r + k;
+    i = i >= kTable ? i - kTable : i;
+    uint32_t s = i + kGap;
+    s = s >= kTable ? s - kTable : s;
+    uint64_t w = tab[i] + tab[s];
+    tab[i] = w;
+    return w;
+}
+
+// Shared-memory control block of one pool.
+struct Ctl {
+    LfgParams cur;   // uniform-generator part of the next pass's parameters
+    LfgParams cur2;  // second slot: the smem engine double-buffers (cur, cur2)
+    double c0d, c1d; // coefficients: n=2 (c*scale, s*scale); n=4 (scale/2, scale)
+    float c0f, c1f;
+    double target;
+    double scale;
+    double tracked;  // pool scalars of the live buffer
+    double withheld;
+    double prev_tracked, prev_withheld;
+    uint64_t draws;
+    uint32_t r;
+    uint32_t active;
+    int32_t error;
+    uint32_t have_prev;
+};
+
+// Generates `total` words in steps of `step` (<= 256, <= blockDim) into
+// wbuf; fn(base, cnt) runs on all threads after each step.
+template <typename F>
+__device__ void lfg_bulk(uint64_t* tab, Ctl* ctl, uint64_t* wbuf, uint64_t total,
+                         uint32_t step, F fn) {
+    uint32_t r = ctl->r;
+    for (uint64_t base = 0; base < total; base += step) {
+        uint32_t cnt = (uint32_t)umin64(step, total - base);
+        if (threadIdx.x < cnt) wbuf[threadIdx.x] = lfg_word_at(tab, r, threadIdx.x);
+        r += cnt;
+        r = r >= kTable ? r - kTable : r;
+        __syncthreads();
+        fn(base, cnt);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) ctl->r = r;
+    __syncthreads();
+}
+
+// UniformState(seed, stream) (uniform.cpp:23-32): table[i] = splitmix64
+// output i of seed ^ rotl(stream, 32), then 6070 discarded words, draws = 0.
+__device__ inline void lfg_seed(uint64_t* tab, Ctl* ctl, uint64_t* wbuf, uint64_t seed,
+                                uint64_t stream, uint32_t step) {
+    const uint64_t s0 = seed ^ ((stream << 32) | (stream >> 32));
+    for (uint32_t i = threadIdx.x; i < kTable; i += blockDim.x)
+        tab[i] = splitmix64_at(s0 + (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull);
+    if (threadIdx.x == 0) {
+        ctl->r = 0;
+        ctl->draws = 0;
+    }
+    __syncthreads();
+    lfg_bulk(tab, ctl, wbuf, kWarmup, step, [](uint64_t, uint32_t) {});
+    if (threadIdx.x == 0) ctl->draws = 0;
+    __syncthreads();
+}
+
+// Warp 0 (all 32 lanes): draw one pass's K words and derive its uniform-
+// generator parameters into ctl->cur (draw order of wallace.cpp:54-58).
+// Lane k owns word k and writes the field that word decides, so the serial
+// part is one table step.
+template <int NA>
+__device__ __forceinline__ void draw_pass_params_warp(uint64_t* tab, Ctl* ctl, uint64_t*,
+                                                      uint32_t N, int slot = 0) {
+    constexpr int K = PassWords<NA>::K;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t r = ctl->r;
+    const uint64_t w = lane < (uint32_t)K ? lfg_word_at(tab, r, lane) : 0ull;
+    const uint64_t w_next = __shfl_down_sync(0xffffffffu, w, 1);
+    LfgParams& p = slot ? ctl->cur2 : ctl->cur;
+    if (NA == 2) {
+        if (lane == 0) p.stride[0] = nib(w, 2) == 0 ? 3 : 5;
+        if (lane == 1) p.stride[1] = nib(w, 2) == 0 ? 7 : 11;
+        if (lane == 2) p.offset[0] = nib(w, N);
+        if (lane == 3) p.offset[1] = nib(w, N);
+        if (lane == 4) {
+            // rotation_from_uniform: t from word 4, region from word 5
+            // (wallace.cpp:44-49), rotation_from_t (wallace.cpp:33-42)
+            const double kTanLo = 0x1.126145e9ecd56p-2;    // 0.26794919243112270
+            const double kTanSpan = 0x1.3cd3a2c8198e2p-2;  // kTanHi - kTanLo, rounded
+            const double t = kTanLo + kTanSpan * u53(w);
+            const uint32_t region = nib(w_next, 3);
+            const double t2 = t * t;
+            const double c = (1.0 - t2) / (1.0 + t2);
+            const double s = 2.0 * t / (1.0 + t2);
+            p.c = region == 2 ? -c : c;
+            p.s = region == 1 ? -s : s;
+        }
+        if (lane == 6) {
+            p.stride[2] = p.stride[3] = 0;
+            p.offset[2] = p.offset[3] = 0;
+            p.variant = 0;
+            p.pad_ = 0;
+        }
+    } else {
+        // strides from {3,5}, {7,11}, {13,17}, {19,23} (docs/n4_spec.md §2)
+        if (lane < 4) {
+            const uint32_t lo = lane == 0 ? 3 : lane == 1 ? 7 : lane == 2 ? 13 : 19;
+            p.stride[lane] = nib(w, 2) == 0 ? lo : lo + (lane == 0 ? 2 : 4);
+        } else if (lane < 8) {
+            p.offset[lane - 4] = nib(w, N);
+        } else if (lane == 8) {
+            p.variant = nib(w, 2);
+        } else if (lane == 9) {
+            p.c = 0.0;
+            p.s = 0.0;
+            p.pad_ = 0;
+        }
+    }
+    if (lane == 31) {
+        const uint32_t nr = r + K;
+        ctl->r = nr >= kTable ? nr - kTable : nr;
+        ctl->draws += K;
+    }
+    __syncwarp();
+}
+
+// Sequential sum of squares in Pool::direct_sumsq order (wallace.cpp:13-18).
+template <typename T>
+__device__ double seq_sumsq(const T* v, uint32_t n) {
+    double q = 0.0;
+#pragma unroll 8
+    for (uint32_t i = 0; i < n; ++i) {
+        double d = (double)v[i];
+        q = q + d * d;
+    }
+    return q;
+}
+
+// init_pool (wallace.cpp:158-167) into `pool` (shared or global): Box-Muller
+// pairs fill arrays 0..n-1 in order, then withheld = .x of one more pair;
+// tracked = sequential sum.  Consumes n*N + 2 uniforms.
+template <typename T>
+__device__ void init_pool_dev(T* pool, uint64_t nvals, uint64_t* tab, Ctl* ctl,
+                              uint64_t* wbuf, uint32_t step) {
+    lfg_bulk(tab, ctl, wbuf, nvals + 2, step, [&](uint64_t base, uint32_t cnt) {
+        for (uint32_t k = threadIdx.x; k < cnt / 2; k += blockDim.x) {
+            double x, y;
+            box_muller(wbuf[2 * k], wbuf[2 * k + 1], x, y);
+            uint64_t i = base + 2 * k;
+            if (i < nvals) {
+                // fill_from_pairs: out = mu + sigma * z with mu = 0, sigma = 1
+                pool[i] = (T)(x + 0.0);
+                pool[i + 1] = (T)(y + 0.0);
+            } else {
+                ctl->withheld = x;
+            }
+        }
+    });
+    if (threadIdx.x == 0) {
+        ctl->draws += nvals + 2;
+        ctl->tracked = seq_sumsq(pool, (uint32_t)nvals);
+    }
+    __syncthreads();
+}
+
+}  // namespace wg

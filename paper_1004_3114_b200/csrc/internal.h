@@ -85,6 +85,9 @@ bool smem_engine_fits(uint32_t n_arrays, uint32_t dtype, uint32_t N);
 EngineShape smem_engine_shape(uint32_t n_arrays, uint32_t dtype, uint32_t N);
 cudaError_t launch_smem(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
                         cudaStream_t st);
+// Probes the dynamic shared-memory base of the current device once (the
+// aligned pool layout needs its low bits to be 0x400).
+void smem_engine_probe(cudaStream_t st);
 
 // HBM engine: one grid-wide launch per pass.
 struct HbmPass {
