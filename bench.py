@@ -243,15 +243,20 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     from paper_1004_3114_b200 import WallaceConfig, WallaceState
 
+    from paper_1004_3114_b200.sharding import shard
+
     c = dict(CONFIGS[cfgname])
     total = args.total or c["total"]
     if cfgname == "c4":
-        seed = c["seed"] + rank
-        per_gpu = total // world
+        # 2^36 normals in total split evenly; GPU g seeded 99 + g (strong scaling)
+        sh = shard(total, world, rank, c["seed"])
+        seed, per_gpu = sh.seed, sh.count
+        scaling = "strong"
     else:
-        seed = c["seed"] if world == 1 else c["seed"] + rank
-        per_gpu = total if world == 1 else total  # weak scaling for c1..c3 at N > 1
-    scaling = "strong" if cfgname == "c4" else "weak"
+        # c1..c3 at N > 1: every GPU runs the whole config on its own seed
+        seed = c["seed"] + (rank if world > 1 else 0)
+        per_gpu = total
+        scaling = "weak"
     out_dtype = torch.float32 if c["dtype"] == "f32" else torch.float64
     esize = 4 if c["dtype"] == "f32" else 8
 
@@ -307,7 +312,7 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         elapsed_ms = float(t.item())
     ms_per_step = elapsed_ms / args.steps
-    total_normals = per_gpu * world
+    total_normals = total if cfgname == "c4" else per_gpu * world
     value = total_normals / (ms_per_step / 1e3)
 
     # Roofline of the dominant kernel: one fill kernel per slab (smem engine),
