@@ -636,7 +636,7 @@ wrng_gpu_status alloc_handle(const wrng_gpu_config* cfg, wrng_gpu** out) {
     CK(cudaMalloc(&g->meta, sizeof(PoolMeta) * cfg->pools));
     CK(cudaMemset(g->meta, 0, sizeof(PoolMeta) * cfg->pools));
     CK(cudaMalloc(&g->lfg, sizeof(LfgState) * cfg->pools));
-    CK(cudaMalloc(&g->scratch, sizeof(double) * 1024));
+    CK(cudaMalloc(&g->scratch, g->hbm ? hbm_drift_scratch_bytes(g->nvals) : sizeof(double) * 1024));
     CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&g->order_ev, cudaEventDisableTiming));

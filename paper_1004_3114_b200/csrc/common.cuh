@@ -296,6 +296,153 @@ __device__ double seq_sumsq(const T* v, uint32_t n) {
     return q;
 }
 
+// ---------------------------------------------------------------------------
+// Exact parallel reproduction of the reference's left-to-right sum of squares
+// (Pool::direct_sumsq, wallace.cpp:13-18: q <- fl(q + v*v), arrays in order).
+//
+// While q stays in one binade [2^E, 2^(E+1)), q is a multiple of
+// u = 2^(E-52) and fl(q + p) = q + u * R with R = p/u rounded to nearest,
+// ties to the even value of q/u + R.  So a chunk of terms adds an INTEGER
+// K = sum R to Q = q/u, exactly, as long as Q + K < 2^53.  R depends on the
+// running parity of Q only at exact ties, and after a tie Q is even whatever
+// came before; hence a chunk's effect is fully described by (K, parity out)
+// for each of the two possible start parities.  These "segment functions"
+// compose associatively.  A single thread then walks the chunks in order,
+// applying each in O(1) when the exact running q is in the chunk's guessed
+// binade and stays there, and adding that chunk's terms one by one
+// otherwise (only near powers of two).  The result is bit-identical to the
+// sequential loop for any inputs (all terms are >= 0).
+// ---------------------------------------------------------------------------
+struct SumSeg {
+    long long s[2];    // K for start parity 0 / 1
+    uint32_t par[2];   // parity after the chunk for start parity 0 / 1
+    uint32_t valid;    // every term satisfied p/u < 2^53
+    int32_t e;         // binade exponent the chunk was evaluated in
+};
+
+__device__ __forceinline__ double pow2d(int e) {  // 2^e for normal e
+    return __longlong_as_double((long long)(e + 1023) << 52);
+}
+__device__ __forceinline__ int exp2_of(double q) {  // floor(log2 q), q normal > 0
+    return (int)((__double_as_longlong(q) >> 52) & 0x7FF) - 1023;
+}
+
+__device__ __forceinline__ void seg_init(SumSeg& g, int e) {
+    g.s[0] = g.s[1] = 0;
+    g.par[0] = 0;
+    g.par[1] = 1;
+    g.valid = 1;
+    g.e = e;
+}
+
+// Appends one term p (>= 0); sc = 2^(52 - e).
+__device__ __forceinline__ void seg_push(SumSeg& g, double p, double sc) {
+    const double x = p * sc;  // exact: scaling by a power of two
+    if (!(x < 0x1.0p53)) {
+        g.valid = 0;
+        return;
+    }
+    const long long k = (long long)x;
+    const double f = x - (double)k;  // exact
+    if (f != 0.5) {
+        const long long r = k + (f > 0.5 ? 1 : 0);
+        g.s[0] += r;
+        g.s[1] += r;
+        g.par[0] ^= (uint32_t)(r & 1);
+        g.par[1] ^= (uint32_t)(r & 1);
+    } else {  // tie: round Q + k + 1/2 to even
+        g.s[0] += k + ((g.par[0] ^ (uint32_t)k) & 1u);
+        g.s[1] += k + ((g.par[1] ^ (uint32_t)k) & 1u);
+        g.par[0] = g.par[1] = 0;
+    }
+}
+
+// a then b (both evaluated in the same binade).
+__device__ __forceinline__ SumSeg seg_compose(const SumSeg& a, const SumSeg& b) {
+    SumSeg c;
+    c.e = a.e;
+    c.valid = a.valid & b.valid & (a.e == b.e ? 1u : 0u);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        c.s[h] = a.s[h] + b.s[a.par[h]];
+        c.par[h] = b.par[a.par[h]];
+    }
+    return c;
+}
+
+// Applies a chunk to the exact running sum q; false when it cannot (q not in
+// the chunk's binade, an invalid term, or the binade would be left).
+__device__ __forceinline__ bool seg_apply(double& q, const SumSeg& g) {
+    if (!g.valid || !(q > 0.0) || exp2_of(q) != g.e) return false;
+    const long long Q = (long long)(q * pow2d(52 - g.e));  // exact integer < 2^53
+    const long long Qn = Q + g.s[Q & 1];
+    if (Qn >= (1ll << 53)) return false;
+    q = (double)Qn * pow2d(g.e - 52);  // exact
+    return true;
+}
+
+template <typename T>
+__device__ __forceinline__ double sq_term(T v) {
+    const double d = (double)v;
+    return d * d;
+}
+
+// CTA-cooperative exact direct_sumsq of v[0, n) (shared or global memory).
+// Uses min(blockDim, 64) chunks; `scratch` (shared) needs 32 bytes per
+// chunk (2 KiB).  Must be called by all threads; returns the sum to all.
+constexpr uint32_t kSumScratchBytes = 64 * sizeof(SumSeg);
+
+template <typename T>
+__device__ double exact_sumsq_cta(const T* v, uint32_t n, void* scratch) {
+    const uint32_t nch = blockDim.x < 64 ? blockDim.x : 64;
+    uint32_t c = n / nch;  // odd chunk length: conflict-free shared reads
+    if (c > 1 && (c & 1) == 0) c -= 1;
+    SumSeg* seg = static_cast<SumSeg*>(scratch);
+    double* pref = static_cast<double*>(scratch);  // aliases seg[], used first
+    const uint32_t t = threadIdx.x;
+    const uint32_t lo = t * c, hi = t + 1 == nch ? n : (t + 1) * c;
+    // pass 1: approximate chunk sums -> exclusive prefix (binade guesses)
+    double a = 0.0;
+    if (t < nch)
+        for (uint32_t i = lo; i < hi; ++i) a += sq_term(v[i]);
+    __syncthreads();
+    if (t < nch) pref[t] = a;
+    __syncthreads();
+    int e = -2000;
+    if (t < nch) {
+        double pre = 0.0;
+        for (uint32_t j = 0; j < t; ++j) pre += pref[j];
+        if (pre > 0.0) e = exp2_of(pre);
+    }
+    // pass 2: segment function of the chunk in its guessed binade
+    SumSeg g;
+    seg_init(g, e);
+    if (t < nch && e > -1000) {
+        const double sc = pow2d(52 - e);
+        for (uint32_t i = lo; i < hi; ++i) seg_push(g, sq_term(v[i]), sc);
+    } else {
+        g.valid = 0;
+    }
+    __syncthreads();
+    if (t < nch) seg[t] = g;
+    __syncthreads();
+    // walk (one thread): O(1) per chunk, term by term only where needed
+    double q = 0.0;
+    if (t == 0) {
+        for (uint32_t k = 0; k < nch; ++k) {
+            if (seg_apply(q, seg[k])) continue;
+            const uint32_t l2 = k * c, h2 = k + 1 == nch ? n : (k + 1) * c;
+            for (uint32_t i = l2; i < h2; ++i) q = q + sq_term(v[i]);
+        }
+    }
+    __syncthreads();
+    if (t == 0) pref[0] = q;
+    __syncthreads();
+    q = pref[0];
+    __syncthreads();
+    return q;
+}
+
 // init_pool (wallace.cpp:158-167) into `pool` (shared or global): Box-Muller
 // pairs fill arrays 0..n-1 in order, then withheld = .x of one more pair;
 // tracked = sequential sum.  Consumes n*N + 2 uniforms.
@@ -316,9 +463,11 @@ __device__ void init_pool_dev(T* pool, uint64_t nvals, uint64_t* tab, Ctl* ctl,
             }
         }
     });
+    // tracked = direct_sumsq (exact left-to-right value, computed in parallel)
+    const double q = exact_sumsq_cta(pool, (uint32_t)nvals, wbuf);
     if (threadIdx.x == 0) {
         ctl->draws += nvals + 2;
-        ctl->tracked = seq_sumsq(pool, (uint32_t)nvals);
+        ctl->tracked = q;
     }
     __syncthreads();
 }

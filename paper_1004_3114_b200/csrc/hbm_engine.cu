@@ -223,24 +223,110 @@ cudaError_t launch_hbm_emit(uint32_t, uint32_t dtype, const KernelArgs& a, uint3
     return cudaGetLastError();
 }
 
-// drift_check on an HBM pool.  Default: one thread, left-to-right, exactly
-// Pool::direct_sumsq (wallace.cpp:13-18).  tree != 0: blocked parallel
-// reduction (documented deviation, relative error ~1e-16 * log n).
+// drift_check on an HBM pool (wallace.cpp:225-234).  Default: the exact
+// value of the left-to-right Pool::direct_sumsq (wallace.cpp:13-18) through
+// the binade segment functions of common.cuh, in four launches:
+//   1 chunk sums (approximate)   2 exclusive scan -> binade guess per chunk
+//   3 segment function per chunk, composed per block of 32 chunks
+//   4 one thread walks blocks, then chunks, then terms where needed.
+// tree != 0: blocked parallel reduction instead (documented deviation,
+// relative error ~1e-16 * log n).
+constexpr uint32_t kSumChunk = 128;
+
 template <typename T>
-__global__ void k_hbm_drift_seq(KernelArgs a, uint32_t buf, uint64_t nvals) {
-    if (a.meta->error || threadIdx.x != 0) return;
+__global__ void k_sum_chunks(KernelArgs a, uint32_t buf, uint64_t nvals, double* approx,
+                             uint32_t nch) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nch || a.meta->error) return;
+    const T* v = static_cast<const T*>(a.buf[buf]);
+    const uint64_t lo = (uint64_t)c * kSumChunk, hi = umin64(lo + kSumChunk, nvals);
+    double s = 0.0;
+    for (uint64_t i = lo; i < hi; ++i) s += sq_term(v[i]);
+    approx[c] = s;
+}
+
+__global__ void __launch_bounds__(1024) k_sum_scan(const double* approx, uint32_t nch,
+                                                   int* e_out, double* pref_scratch) {
+    // approximate exclusive prefix: per-thread serial runs + one block scan
+    __shared__ double part[1024];
+    const uint32_t t = threadIdx.x, per = (nch + 1023) / 1024;
+    const uint32_t lo = t * per, hi = lo + per < nch ? lo + per : nch;
+    double s = 0.0;
+    for (uint32_t i = lo; i < hi; ++i) s += approx[i];
+    part[t] = s;
+    __syncthreads();
+    for (uint32_t off = 1; off < 1024; off <<= 1) {
+        double x = t >= off ? part[t - off] : 0.0;
+        __syncthreads();
+        part[t] += x;
+        __syncthreads();
+    }
+    double pre = t ? part[t - 1] : 0.0;
+    for (uint32_t i = lo; i < hi; ++i) {
+        pref_scratch[i] = pre;
+        e_out[i] = pre > 0.0 ? exp2_of(pre) : -2000;
+        pre += approx[i];
+    }
+}
+
+template <typename T>
+__global__ void k_sum_segs(KernelArgs a, uint32_t buf, uint64_t nvals, const int* e_in,
+                           SumSeg* segs, SumSeg* blocks, uint32_t nch) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    const T* v = static_cast<const T*>(a.buf[buf]);
+    SumSeg g;
+    const int e = c < nch ? e_in[c] : -2000;
+    seg_init(g, e);
+    if (c < nch && e > -1000) {
+        const double sc = pow2d(52 - e);
+        const uint64_t lo = (uint64_t)c * kSumChunk, hi = umin64(lo + kSumChunk, nvals);
+        for (uint64_t i = lo; i < hi; ++i) seg_push(g, sq_term(v[i]), sc);
+    } else {
+        g.valid = 0;
+    }
+    if (c < nch) segs[c] = g;
+    // compose 32 consecutive chunks (lane order) into one block function
+    const uint32_t lane = threadIdx.x & 31u;
+    for (uint32_t off = 1; off < 32; off <<= 1) {
+        SumSeg o;
+        o.s[0] = __shfl_down_sync(0xffffffffu, g.s[0], off);
+        o.s[1] = __shfl_down_sync(0xffffffffu, g.s[1], off);
+        o.par[0] = __shfl_down_sync(0xffffffffu, g.par[0], off);
+        o.par[1] = __shfl_down_sync(0xffffffffu, g.par[1], off);
+        o.valid = __shfl_down_sync(0xffffffffu, g.valid, off);
+        o.e = __shfl_down_sync(0xffffffffu, g.e, off);
+        if ((lane & (2 * off - 1)) == 0) g = seg_compose(g, o);
+    }
+    if (lane == 0 && c < nch) blocks[c / 32] = g;
+}
+
+template <typename T>
+__global__ void k_sum_walk(KernelArgs a, uint32_t buf, uint64_t nvals, const SumSeg* segs,
+                           const SumSeg* blocks, uint32_t nch) {
+    if (threadIdx.x != 0 || a.meta->error) return;
     const T* v = static_cast<const T*>(a.buf[buf]);
     double q = 0.0;
-#pragma unroll 16
-    for (uint64_t i = 0; i < nvals; ++i) {
-        double d = (double)v[i];
-        q = q + d * d;
+    const uint32_t nblk = (nch + 31) / 32;
+    for (uint32_t b = 0; b < nblk; ++b) {
+        if (b * 32 + 32 <= nch && seg_apply(q, blocks[b])) continue;
+        const uint32_t cend = b * 32 + 32 < nch ? b * 32 + 32 : nch;
+        for (uint32_t c = b * 32; c < cend; ++c) {
+            if (seg_apply(q, segs[c])) continue;
+            const uint64_t lo = (uint64_t)c * kSumChunk, hi = umin64(lo + kSumChunk, nvals);
+            for (uint64_t i = lo; i < hi; ++i) q = q + sq_term(v[i]);
+        }
     }
-    double rel = fabs(q / a.meta->tracked[buf] - 1.0);
+    const double rel = fabs(q / a.meta->tracked[buf] - 1.0);
     if (!(rel <= 1e-3))
         a.meta->error = WRNG_GPU_ECORRUPT;
     else
         a.meta->tracked[buf] = q;
+}
+
+size_t hbm_drift_scratch_bytes(uint64_t nvals) {
+    const uint64_t nch = (nvals + kSumChunk - 1) / kSumChunk;
+    return nch * (2 * sizeof(double) + sizeof(int) + sizeof(SumSeg)) +
+           ((nch + 31) / 32) * sizeof(SumSeg) + 1024;
 }
 
 template <typename T>
@@ -278,10 +364,26 @@ cudaError_t launch_hbm_drift(uint32_t n_arrays, uint32_t dtype, const KernelArgs
                              uint32_t buf, int tree, double* scratch, cudaStream_t st) {
     const uint64_t nvals = (uint64_t)n_arrays * a.N;
     if (!tree) {
-        if (dtype == WRNG_GPU_F64)
-            k_hbm_drift_seq<double><<<1, 32, 0, st>>>(a, buf, nvals);
-        else
-            k_hbm_drift_seq<float><<<1, 32, 0, st>>>(a, buf, nvals);
+        const uint32_t nch = (uint32_t)((nvals + kSumChunk - 1) / kSumChunk);
+        char* p = reinterpret_cast<char*>(scratch);
+        double* approx = reinterpret_cast<double*>(p);
+        double* pref = approx + nch;
+        int* e = reinterpret_cast<int*>(pref + nch);
+        SumSeg* segs = reinterpret_cast<SumSeg*>(
+            (reinterpret_cast<uintptr_t>(e + nch) + 63) & ~uintptr_t(63));
+        SumSeg* blocks = segs + nch;
+        const uint32_t g = (nch + 255) / 256;
+        if (dtype == WRNG_GPU_F64) {
+            k_sum_chunks<double><<<g, 256, 0, st>>>(a, buf, nvals, approx, nch);
+            k_sum_scan<<<1, 1024, 0, st>>>(approx, nch, e, pref);
+            k_sum_segs<double><<<g, 256, 0, st>>>(a, buf, nvals, e, segs, blocks, nch);
+            k_sum_walk<double><<<1, 32, 0, st>>>(a, buf, nvals, segs, blocks, nch);
+        } else {
+            k_sum_chunks<float><<<g, 256, 0, st>>>(a, buf, nvals, approx, nch);
+            k_sum_scan<<<1, 1024, 0, st>>>(approx, nch, e, pref);
+            k_sum_segs<float><<<g, 256, 0, st>>>(a, buf, nvals, e, segs, blocks, nch);
+            k_sum_walk<float><<<1, 32, 0, st>>>(a, buf, nvals, segs, blocks, nch);
+        }
         return cudaGetLastError();
     }
     const uint32_t nb = 296;

@@ -106,6 +106,7 @@ cudaError_t launch_hbm_pass(uint32_t n_arrays, uint32_t dtype, const KernelArgs&
 cudaError_t launch_hbm_emit(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
                             uint32_t buf, uint64_t pos, uint64_t take, uint64_t out_off,
                             cudaStream_t st);
+size_t hbm_drift_scratch_bytes(uint64_t nvals);
 cudaError_t launch_hbm_drift(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
                              uint32_t buf, int tree, double* scratch,
                              cudaStream_t st);

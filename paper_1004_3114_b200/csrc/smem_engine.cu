@@ -1,557 +1,14 @@
-// Shared-memory engine: one CTA per pool, the pool resident in shared memory
-// for the whole fill call (BASELINE.json configs C1, C3, C4, C5).
-//
-// One regeneration pass (wallace.cpp:113-137, in the naive modular form the
-// reference pins bit-identical to its segmented loop,
-// tests/test_wallace_core.cpp:203-217) runs IN PLACE in two phases separated
-// by one barrier:
-//   B  gather x_m[(a_m j + g_m) mod N] for this thread's columns j = tid +
-//      k*NTH (lane-consecutive: odd strides hit 32 distinct banks) and form
-//      the unscaled transform — for n = 4 the scale multiply is the last
-//      rounding of every element (docs/n4_spec.md §3), so the Hadamard /
-//      (J/2 - I) sums need no scale.  Thread 0 meanwhile derives this pass's
-//      chi-squared scale from the previous withheld value
-//      (wallace.cpp:62-65).
-//   C  multiply by the scale, store back in place and, on the last pass of a
-//      refill, stream the exposed values to HBM straight from registers
-//      (coalesced 128-byte warp stores at immediate offsets,
-//      wallace.cpp:206-213).  Warp 0 meanwhile draws the next pass's uniform
-//      words (wallace.cpp:54-58), one word per lane.
-//
-// Addressing: pool accesses are 32-bit shared-window addresses.  When one
-// pool array (N * sizeof(T) bytes) is at most 8 KiB the pool is placed on an
-// N*sizeof(T)-aligned shared address, so a gather address is a single LOP3
-// ((idx & mask) | base) plus an immediate array offset in the LDS; the
-// alignment assumption is probed once per device (smem_base_probe) and the
-// IADD form is used otherwise.
-#include <type_traits>
-
-#include "common.cuh"
-
-#ifndef WG_DATA_REGS
-#define WG_DATA_REGS 64  // registers holding one thread's columns of a pass
-#endif
+// Shared-memory engine, host side: dispatch to the per-(dtype, n) kernel
+// instantiations (smem_{f32,f64}_n{2,4}.cu; templates in smem_impl.cuh) and
+// the once-per-device shared-window probe.
+#include "smem_impl.cuh"
 
 namespace wg {
 
-extern __shared__ __align__(16) unsigned char g_sm[];
-
-enum EmitMode : int { EM_UNIT = 0, EM_GENERIC = 1 };
-
-constexpr uint32_t pick_j(uint32_t N, uint32_t regs_per_col) {
-    uint32_t j = WG_DATA_REGS / regs_per_col;
-    if (j > 32) j = 32;
-    while (N / j < 32 && j > 1) j /= 2;
-    while (N / j > 1024) j *= 2;
-    return j;
-}
-
-// The dynamic shared-memory window of a CTA starts 1 KiB in (reserved
-// system area); smem_base_probe() checks this once per device.
-constexpr uint32_t kDynSmemBase = 0x400;
-
-template <typename T, int NA, int LOGN>
-struct SmemShape {
-    static constexpr uint32_t N = 1u << LOGN;
-    static constexpr uint32_t J = pick_j(N, NA * (uint32_t)sizeof(T) / 4);  // columns/thread
-    static constexpr uint32_t NTH = N / J;                                  // CTA size
-    // registers/thread = 65536 / (NTH * MINB): 2*WG_DATA_REGS
-    static constexpr uint32_t MINB =
-        NTH >= 32768 / WG_DATA_REGS ? 1 : (32768 / WG_DATA_REGS) / NTH;
-    static constexpr uint32_t MASK = N - 1;
-    static constexpr uint32_t ABYTES = N * (uint32_t)sizeof(T);  // one array
-    static constexpr uint32_t MASKB = MASK * (uint32_t)sizeof(T);
-    static constexpr uint64_t NVALS = (uint64_t)NA * N;
-    static constexpr uint64_t CAP = NVALS - 1;
-    static constexpr uint32_t STEP = NTH < 256 ? NTH : 256;  // uniform words per bulk step
-    // shared layout: lag table | word staging | control block | pool
-    static constexpr uint32_t TAB_OFF = 0;
-    static constexpr uint32_t WBUF_OFF = 608 * 8;
-    static constexpr uint32_t CTL_OFF = WBUF_OFF + 256 * 8;
-    static constexpr uint32_t HEAD = CTL_OFF + 256;
-    static_assert(sizeof(Ctl) <= 256, "control block");
-    static constexpr bool CAN_ALIGN = ABYTES <= 8192;
-    static constexpr uint32_t POOL_OFF =
-        CAN_ALIGN ? ((kDynSmemBase + HEAD + ABYTES - 1) / ABYTES) * ABYTES - kDynSmemBase
-                  : HEAD;
-    static constexpr uint32_t BYTES = POOL_OFF + (uint32_t)(NVALS * sizeof(T));
-};
-
-template <int B, int E, typename F>
-__device__ __forceinline__ void sfor(F&& f) {
-    if constexpr (B < E) {
-        f(std::integral_constant<int, B>{});
-        sfor<B + 1, E>(f);
-    }
-}
-
-template <typename T, uint32_t OFF>
-__device__ __forceinline__ T lds(uint32_t a) {
-    T v;
-    if constexpr (sizeof(T) == 4)
-        asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"(OFF));
-    else
-        asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(OFF));
-    return v;
-}
-
-template <typename T, uint32_t OFF>
-__device__ __forceinline__ void sts(uint32_t a, T v) {
-    if constexpr (sizeof(T) == 4)
-        asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(a), "n"(OFF), "f"(v) : "memory");
-    else
-        asm volatile("st.shared.f64 [%0+%1], %2;" ::"r"(a), "n"(OFF), "d"(v) : "memory");
-}
-
-template <typename T>
-__device__ __forceinline__ T& sm_at(uint32_t off) {
-    return *reinterpret_cast<T*>(g_sm + off);
-}
-
-template <typename T, int EM>
-__device__ __forceinline__ void emit_one(void* out, uint64_t i, T v, uint32_t out_f32,
-                                         uint32_t unit, double mu, double sigma) {
-    if (EM == EM_UNIT)
-        static_cast<T*>(out)[i] = v + (T)0;  // 0 + 1 * v: -0.0 -> +0.0
-    else
-        put_out(out, i, v, out_f32, unit, mu, sigma);
-}
-
-struct EmitCfg {  // per-launch constants of the output stream
-    double mu, sigma;
-    uint32_t out_f32, unit;
-};
-
-// Phase B: gather + unscaled transform (VAR = n=4 matrix variant; AL =
-// aligned pool base, gather address = (idx & mask) | base).
-template <typename T, int NA, int LOGN, int VAR, bool AL>
-__device__ __forceinline__ void phase_b(uint32_t pool_s, uint32_t (&ixb)[NA],
-                                        const uint32_t (&stepb)[NA],
-                                        T (&u)[NA][SmemShape<T, NA, LOGN>::J]) {
-    using S = SmemShape<T, NA, LOGN>;
-    sfor<0, (int)S::J>([&](auto kc) {
-        constexpr int k = decltype(kc)::value;
-        T g[NA];
-        sfor<0, NA>([&](auto mc) {
-            constexpr int m = decltype(mc)::value;
-            const uint32_t a =
-                AL ? ((ixb[m] & S::MASKB) | pool_s) : ((ixb[m] & S::MASKB) + pool_s);
-            g[m] = lds<T, (uint32_t)m * S::ABYTES>(a);
-            ixb[m] += stepb[m];
-        });
-        if constexpr (NA == 4) {
-            if constexpr (VAR == 0) {
-                // (1/2) H4: y = k * {(p+r), (q+s), (p-r), (q-s)}
-                const T pp = g[0] + g[1], q = g[0] - g[1], r = g[2] + g[3], s = g[2] - g[3];
-                u[0][k] = pp + r;
-                u[1][k] = q + s;
-                u[2][k] = pp - r;
-                u[3][k] = q - s;
-            } else {
-                // (1/2) J - I: y_i = scale * (t - x_i)
-                const T t = (T)0.5 * ((g[0] + g[1]) + (g[2] + g[3]));
-                u[0][k] = t - g[0];
-                u[1][k] = t - g[1];
-                u[2][k] = t - g[2];
-                u[3][k] = t - g[3];
-            }
-        } else {
-            u[0][k] = g[0];
-            u[1][k] = g[1];
-        }
-    });
-}
-
-// Phase C: scale, store in place, emit.  MD 0: no emission; 1: the whole
-// exposed pool (all but the withheld slot) with unit output: unconditional
-// stores at immediate offsets; 2: partial window / generic output.
-template <typename T, int NA, int LOGN, int EM, int MD>
-__device__ __forceinline__ void phase_c(const T (&u)[NA][SmemShape<T, NA, LOGN>::J], T c0, T c1,
-                                        uint32_t pool_s, char* out_p, uint32_t en,
-                                        const EmitCfg& ec, double& withheld_out) {
-    using S = SmemShape<T, NA, LOGN>;
-    const uint32_t tid = threadIdx.x;
-    const uint32_t my_s = pool_s + tid * (uint32_t)sizeof(T);
-    T* ob = MD == 1 ? reinterpret_cast<T*>(out_p) + tid : nullptr;
-    sfor<0, (int)S::J>([&](auto kc) {
-        constexpr int k = decltype(kc)::value;
-        T y[NA];
-        if constexpr (NA == 4) {
-#pragma unroll
-            for (int m = 0; m < NA; ++m) y[m] = c0 * u[m][k];
-        } else {
-            // dst.x = kc*xs + ks*ys ; dst.y = kc*ys - ks*xs (wallace.cpp:130-131)
-            const T xs = u[0][k], ys = u[1][k];
-            y[0] = c0 * xs + c1 * ys;
-            y[1] = c0 * ys - c1 * xs;
-        }
-        sfor<0, NA>([&](auto mc) {
-            constexpr int m = decltype(mc)::value;
-            constexpr uint32_t col = m * S::N + k * S::NTH;
-            sts<T, col * (uint32_t)sizeof(T)>(my_s, y[m]);
-            if constexpr (MD == 1) {
-                if (!(m == NA - 1 && k == (int)S::J - 1) || tid != S::NTH - 1)
-                    ob[col] = y[m] + (T)0;  // 0 + 1 * v
-            } else if constexpr (MD == 2) {
-                const uint32_t flat = col + tid;
-                if (flat < en)
-                    emit_one<T, EM>(out_p, flat, y[m], ec.out_f32, ec.unit, ec.mu, ec.sigma);
-            }
-        });
-        if (k == (int)S::J - 1 && tid == S::NTH - 1) withheld_out = (double)y[NA - 1];
-    });
-}
-
-// One in-place regeneration pass.  Preconditions (after a barrier): the
-// parameter slot `slot` (ctl->cur / ctl->cur2) holds this pass's uniform-
-// generator parameters.  prefetch: warp 0 draws the next pass's words into
-// the other slot during phase B.  prev: when non-null, the pre-pass pool is
-// copied there (it becomes the inactive buffer).  Returns false on a
-// device-detected error (ctl->error set); every thread returns the same.
-//
-// The chi-squared scale (wallace.cpp:59-69) is derived by EVERY thread from
-// the broadcast (tracked, withheld): warp-uniform, so its fp64 div/sqrt
-// chain overlaps the gathers instead of serialising one lane of warp 0.
-template <typename T, int NA, int LOGN, int EM, bool AL>
-__device__ __forceinline__ bool smem_pass(uint32_t pool_s, uint32_t mode, uint32_t emit_n,
-                                          char* out_p, const EmitCfg& ec, wrng_gpu_params* rec,
-                                          bool prefetch, T* prev, int slot) {
-    using S = SmemShape<T, NA, LOGN>;
-    constexpr uint32_t N = S::N, NTH = S::NTH;
-    const uint32_t tid = threadIdx.x;
-    Ctl* ctl = &sm_at<Ctl>(S::CTL_OFF);
-    const LfgParams& cp = slot ? ctl->cur2 : ctl->cur;
-
-    uint32_t ixb[NA], stepb[NA];
-#pragma unroll
-    for (int m = 0; m < NA; ++m) {
-        const uint32_t st = cp.stride[m];
-        ixb[m] = (st * tid + cp.offset[m]) * (uint32_t)sizeof(T);
-        stepb[m] = st * NTH * (uint32_t)sizeof(T);
-    }
-    const uint32_t variant = cp.variant;
-    const double tracked = ctl->tracked, withheld = ctl->withheld;
-    double scale = 0.0, target = 0.0;
-    const int e = pass_scale(tracked, withheld, (uint32_t)S::NVALS, mode, scale, target);
-    // regenerate folds the scale into the matrix (wallace.cpp:116-117)
-    const double c0d = NA == 2 ? cp.c * scale : (variant ? scale : 0.5 * scale);
-    const double c1d = NA == 2 ? cp.s * scale : scale;
-    if (tid == 0) {
-        ctl->error = e;
-        if (!e && rec) {
-#pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                rec->stride[m] = cp.stride[m];
-                rec->offset[m] = cp.offset[m];
-            }
-            rec->variant = cp.variant;
-            rec->pad_ = 0;
-            rec->c = cp.c;
-            rec->s = cp.s;
-            rec->scale = scale;
-            rec->target_sumsq = target;
-        }
-        if (prev && !e) {
-            ctl->prev_tracked = tracked;
-            ctl->prev_withheld = withheld;
-            ctl->have_prev = 1;
-        }
-    }
-    if (e) {
-        __syncthreads();
-        return false;
-    }
-    if (prev) {
-        // the pre-pass pool becomes the inactive buffer (wallace.cpp:170-174)
-        constexpr uint32_t NVEC = (uint32_t)(S::NVALS * sizeof(T) / 16);
-        uint4* dst = reinterpret_cast<uint4*>(prev);
-        for (uint32_t i = tid; i < NVEC; i += NTH) dst[i] = sm_at<uint4>(S::POOL_OFF + i * 16);
-    }
-    if (prefetch && tid < 32)
-        draw_pass_params_warp<NA>(&sm_at<uint64_t>(S::TAB_OFF), ctl,
-                                  &sm_at<uint64_t>(S::WBUF_OFF), N, slot ^ 1);
-    T u[NA][S::J];
-    if (NA == 2 || variant == 0)
-        phase_b<T, NA, LOGN, 0, AL>(pool_s, ixb, stepb, u);
-    else
-        phase_b<T, NA, LOGN, 1, AL>(pool_s, ixb, stepb, u);
-    __syncthreads();
-
-    const T c0 = (T)c0d, c1 = (T)c1d;  // fp32 pools: rounded once (docs/n4_spec.md §4)
-    double wh = 0.0;
-    if (emit_n == 0)
-        phase_c<T, NA, LOGN, EM, 0>(u, c0, c1, pool_s, out_p, 0, ec, wh);
-    else if (EM == EM_UNIT && emit_n == (uint32_t)S::CAP)
-        phase_c<T, NA, LOGN, EM, 1>(u, c0, c1, pool_s, out_p, emit_n, ec, wh);
-    else
-        phase_c<T, NA, LOGN, EM, 2>(u, c0, c1, pool_s, out_p, emit_n, ec, wh);
-    if (tid == NTH - 1) ctl->withheld = wh;  // wallace.cpp:136
-    if (tid == 0) {
-        ctl->tracked = target;  // wallace.cpp:135
-        ctl->active ^= 1u;
-    }
-    __syncthreads();
-    return true;
-}
-
-template <typename T, int NA, int LOGN>
-__device__ __forceinline__ bool smem_drift_check() {
-    // wallace.cpp:225-234 with Pool::direct_sumsq order (wallace.cpp:13-18)
-    using S = SmemShape<T, NA, LOGN>;
-    Ctl* ctl = &sm_at<Ctl>(S::CTL_OFF);
-    if (threadIdx.x == 0) {
-        const double rec = seq_sumsq(&sm_at<T>(S::POOL_OFF), (uint32_t)S::NVALS);
-        const double rel = fabs(rec / ctl->tracked - 1.0);
-        if (!(rel <= 1e-3))
-            ctl->error = WRNG_GPU_ECORRUPT;
-        else
-            ctl->tracked = rec;
-    }
-    __syncthreads();
-    return ctl->error == 0;
-}
-
-template <typename T, int NA, int LOGN>
-__device__ __forceinline__ void smem_restart() {
-    using S = SmemShape<T, NA, LOGN>;
-    init_pool_dev(&sm_at<T>(S::POOL_OFF), S::NVALS, &sm_at<uint64_t>(S::TAB_OFF),
-                  &sm_at<Ctl>(S::CTL_OFF), &sm_at<uint64_t>(S::WBUF_OFF), S::STEP);
-}
-
-// Passes-until-boundary bookkeeping without divisions in the refill loop:
-// crossed(before, before + f, P) (wallace.cpp:182-184) <=> (before mod P) + f >= P.
-struct PeriodCounter {
-    uint64_t period, rem;
-    __device__ __forceinline__ void init(uint64_t P, uint64_t pc) {
-        period = P;
-        rem = P ? pc % P : 0;
-    }
-    __device__ __forceinline__ bool will_cross(uint64_t f) const {
-        return period > 0 && rem + f >= period;
-    }
-    __device__ __forceinline__ void advance(uint64_t f) {
-        if (!period) return;
-        rem += f;
-        while (rem >= period) rem -= period;
-    }
-};
-
-template <typename T, int NA, int LOGN, int EM, bool AL>
-__global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, LOGN>::MINB)
-    k_smem(const KernelArgs a) {
-    using S = SmemShape<T, NA, LOGN>;
-    constexpr uint32_t N = S::N, NTH = S::NTH;
-    constexpr uint64_t NVALS = S::NVALS, CAP = S::CAP;
-
-    uint64_t* tab = &sm_at<uint64_t>(S::TAB_OFF);
-    uint64_t* wbuf = &sm_at<uint64_t>(S::WBUF_OFF);
-    Ctl* ctl = &sm_at<Ctl>(S::CTL_OFF);
-    const uint32_t pool_s = (uint32_t)__cvta_generic_to_shared(g_sm) + S::POOL_OFF;
-
-    const uint32_t tid = threadIdx.x;
-    const uint32_t p = blockIdx.x;
-    PoolMeta* meta = a.meta + p;
-    LfgState* lg = a.lfg + p;
-    const uint32_t op = a.op;
-    // A device-raised error is sticky until the host observes it: the pool
-    // stays frozen at the failure point.
-    if (op != OP_INIT && meta->error) return;
-
-    // ---- load state -------------------------------------------------------
-    uint64_t pc, avail, emitted;
-    if (op == OP_INIT) {
-        pc = avail = emitted = 0;
-        if (tid == 0) {
-            ctl->active = 0;
-            ctl->error = 0;
-            ctl->have_prev = 0;
-        }
-        lfg_seed(tab, ctl, wbuf, a.seed, a.stream0 + p, S::STEP);
-    } else {
-        pc = meta->pass_count;
-        avail = meta->avail;
-        emitted = meta->emitted;
-        const uint32_t act = meta->active;
-        for (uint32_t i = tid; i < kTable; i += NTH) tab[i] = lg->table[i];
-        if (tid == 0) {
-            ctl->r = lg->r;
-            ctl->draws = lg->draws;
-            ctl->active = act;
-            ctl->tracked = meta->tracked[act];
-            ctl->withheld = meta->withheld[act];
-            ctl->error = 0;
-            ctl->have_prev = 0;
-        }
-        const uint4* src = reinterpret_cast<const uint4*>(static_cast<const T*>(a.buf[act]) +
-                                                          (uint64_t)p * NVALS);
-        constexpr uint32_t NVEC = (uint32_t)(NVALS * sizeof(T) / 16);
-        for (uint32_t i = tid; i < NVEC; i += NTH) sm_at<uint4>(S::POOL_OFF + i * 16) = src[i];
-    }
-    __syncthreads();
-
-    const uint64_t len = a.lay.len_base + (p < a.lay.len_extra ? 1 : 0);
-    const uint64_t out_base =
-        (uint64_t)p * a.lay.off_stride + (p < a.lay.off_extra ? p : a.lay.off_extra);
-    const uint32_t f = a.f;
-    const uint32_t mode = a.mode;
-    const EmitCfg ec{a.mu, a.sigma, a.out_f32, a.unit};
-    PeriodCounter drift, restart;
-    drift.init(a.drift, pc);
-    restart.init(a.restart, pc);
-
-    // ---- passes in this launch (the last one keeps its source pool as the
-    // inactive buffer, as advance_pass's swap does, wallace.cpp:170-174) ---
-    uint64_t total_passes = 0;
-    if (op == OP_FILL) {
-        uint64_t rem = len;
-        if (avail > 0 && rem > 0) rem -= umin64(rem, avail);
-        if (a.restart == 0) {
-            total_passes = (rem + CAP - 1) / CAP * f;
-        } else {
-            PeriodCounter r2 = restart;
-            while (rem > 0) {
-                const bool rs = r2.will_cross(f);
-                r2.advance(f);
-                total_passes += f;
-                if (rs) continue;
-                rem -= umin64(rem, CAP);
-            }
-        }
-    } else if (op == OP_PASSES) {
-        total_passes = a.npasses;
-    } else if (op == OP_REFILL) {
-        total_passes = f;
-    }
-
-    uint64_t pass_i = 0;
-    bool primed = false;  // parameter slot `slot` holds the next pass's parameters
-    int slot = 0;
-    int err = 0;
-    char* outc = static_cast<char*>(a.out);
-    const uint32_t esz = EM == EM_UNIT ? (uint32_t)sizeof(T) : (a.out_f32 ? 4u : 8u);
-
-    auto prev_buf = [&]() -> T* {
-        return static_cast<T*>(a.buf[ctl->active]) + (uint64_t)p * NVALS;
-    };
-
-    uint64_t done = 0;
-    if (op == OP_FILL && avail > 0 && len > 0) {
-        // leftover of the live pool: flat [pos, pos + take)
-        const uint64_t take = umin64(len, avail);
-        const uint64_t pos = CAP - avail;
-        char* o = outc + out_base * esz;
-        const T* pl = &sm_at<T>(S::POOL_OFF);
-        for (uint64_t i = tid; i < take; i += NTH)
-            emit_one<T, EM>(o, i, pl[pos + i], ec.out_f32, ec.unit, ec.mu, ec.sigma);
-        done = take;
-        avail -= take;
-    }
-    bool once = op == OP_REFILL;
-    while (!err && ((op == OP_FILL && done < len) || once)) {
-        once = false;
-        // refill (wallace.cpp:188-196), the exposed window fused into the
-        // last pass.
-        const bool will_restart = restart.will_cross(f);
-        const bool will_drift = drift.will_cross(f);
-        const uint64_t want = op == OP_FILL ? umin64(len - done, CAP) : 0;
-        const uint32_t emit_n = will_restart ? 0u : (uint32_t)want;
-        char* out_p = outc + (out_base + done) * esz;
-        for (uint32_t i = 0; i < f; ++i) {
-            const bool lastp = i + 1 == f;
-            if (!primed) {
-                if (tid < 32) draw_pass_params_warp<NA>(tab, ctl, wbuf, N, slot);
-                __syncthreads();
-            }
-            ++pass_i;
-            const bool last_launch = pass_i == total_passes;
-            const bool prefetch = !last_launch && !(lastp && will_restart);
-            if (!smem_pass<T, NA, LOGN, EM, AL>(pool_s, mode, lastp ? emit_n : 0u, out_p, ec,
-                                                nullptr, prefetch,
-                                                last_launch ? prev_buf() : nullptr, slot)) {
-                err = ctl->error;
-                break;
-            }
-            primed = prefetch;
-            if (prefetch) slot ^= 1;
-            ++pc;
-        }
-        if (err) break;
-        restart.advance(f);
-        drift.advance(f);
-        avail = CAP;
-        if (will_drift && !smem_drift_check<T, NA, LOGN>()) {
-            err = ctl->error;
-            break;
-        }
-        if (will_restart) {
-            smem_restart<T, NA, LOGN>();
-            avail = 0;
-            primed = false;
-            continue;
-        }
-        done += emit_n;
-        avail -= emit_n;
-    }
-    if (op == OP_FILL && !err) emitted += len;
-    if (op == OP_PASSES) {
-        for (uint32_t i = 0; i < a.npasses && !err; ++i) {
-            // advance_pass (wallace.cpp:169-178)
-            if (!primed) {
-                if (tid < 32) draw_pass_params_warp<NA>(tab, ctl, wbuf, N, slot);
-                __syncthreads();
-            }
-            ++pass_i;
-            const bool last_launch = pass_i == total_passes;
-            wrng_gpu_params* rec = (a.params_out && last_launch) ? a.params_out + p : nullptr;
-            if (!smem_pass<T, NA, LOGN, EM, AL>(pool_s, mode, 0u, nullptr, ec, rec,
-                                                !last_launch,
-                                                last_launch ? prev_buf() : nullptr, slot)) {
-                err = ctl->error;
-                break;
-            }
-            primed = !last_launch;
-            if (primed) slot ^= 1;
-            ++pc;
-            avail = 0;
-        }
-    }
-    if (op == OP_DRIFT) {
-        if (!smem_drift_check<T, NA, LOGN>()) err = ctl->error;
-    } else if (op == OP_RESTART || op == OP_INIT) {
-        smem_restart<T, NA, LOGN>();
-        avail = 0;
-    }
-
-    // ---- write back -------------------------------------------------------
-    __syncthreads();
-    const uint32_t act = ctl->active;
-    {
-        uint4* dst =
-            reinterpret_cast<uint4*>(static_cast<T*>(a.buf[act]) + (uint64_t)p * NVALS);
-        constexpr uint32_t NVEC = (uint32_t)(NVALS * sizeof(T) / 16);
-        for (uint32_t i = tid; i < NVEC; i += NTH) dst[i] = sm_at<uint4>(S::POOL_OFF + i * 16);
-    }
-    for (uint32_t i = tid; i < kTable; i += NTH) lg->table[i] = tab[i];
-    if (tid == 0) {
-        lg->r = ctl->r;
-        lg->draws = ctl->draws;
-        meta->tracked[act] = ctl->tracked;
-        meta->withheld[act] = ctl->withheld;
-        if (ctl->have_prev) {
-            meta->tracked[act ^ 1u] = ctl->prev_tracked;
-            meta->withheld[act ^ 1u] = ctl->prev_withheld;
-        }
-        if (op == OP_INIT) {
-            meta->tracked[1] = 0.0;
-            meta->withheld[1] = 0.0;
-        }
-        meta->active = act;
-        meta->pass_count = pc;
-        meta->avail = avail;
-        meta->emitted = emitted;
-        meta->error = (uint32_t)err;
-    }
-}
+cudaError_t smem_dispatch_f32_n2(const KernelArgs&, cudaStream_t, bool, bool);
+cudaError_t smem_dispatch_f32_n4(const KernelArgs&, cudaStream_t, bool, bool);
+cudaError_t smem_dispatch_f64_n2(const KernelArgs&, cudaStream_t, bool, bool);
+cudaError_t smem_dispatch_f64_n4(const KernelArgs&, cudaStream_t, bool, bool);
 
 __global__ void k_smem_base_probe(uint32_t* out) {
     if (threadIdx.x == 0) *out = (uint32_t)__cvta_generic_to_shared(g_sm) & 0xFFFFFFu;
@@ -560,7 +17,6 @@ __global__ void k_smem_base_probe(uint32_t* out) {
 // ---------------------------------------------------------------------------
 // Host-side dispatch
 // ---------------------------------------------------------------------------
-static constexpr uint32_t kSmemPoolMax = 128 * 1024;  // largest pool kept on chip
 
 // Low 24 bits of the dynamic shared-memory base per device (-1: unknown).
 static int64_t g_base_low[64];
@@ -607,62 +63,16 @@ EngineShape smem_engine_shape(uint32_t n_arrays, uint32_t dtype, uint32_t N) {
     return s;
 }
 
-template <typename T, int NA, int LOGN, int EM, bool AL>
-static cudaError_t go(const KernelArgs& a, cudaStream_t st) {
-    using S = SmemShape<T, NA, LOGN>;
-    auto kern = k_smem<T, NA, LOGN, EM, AL>;
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
-    if (e != cudaSuccess) return e;
-    kern<<<a.pools, S::NTH, S::BYTES, st>>>(a);
-    return cudaGetLastError();
-}
-
-template <typename T, int NA, int LOGN>
-static cudaError_t go_em(const KernelArgs& a, cudaStream_t st, bool unit_same, bool al) {
-    using S = SmemShape<T, NA, LOGN>;
-    if constexpr (S::CAN_ALIGN) {
-        if (al)
-            return unit_same ? go<T, NA, LOGN, EM_UNIT, true>(a, st)
-                             : go<T, NA, LOGN, EM_GENERIC, true>(a, st);
-    }
-    return unit_same ? go<T, NA, LOGN, EM_UNIT, false>(a, st)
-                     : go<T, NA, LOGN, EM_GENERIC, false>(a, st);
-}
-
-template <typename T, int NA>
-static cudaError_t dispatch(const KernelArgs& a, cudaStream_t st, bool unit_same, bool al) {
-    constexpr uint32_t es = sizeof(T);
-    switch (a.N) {
-        case 1u << 8: return go_em<T, NA, 8>(a, st, unit_same, al);
-        case 1u << 9: return go_em<T, NA, 9>(a, st, unit_same, al);
-        case 1u << 10: return go_em<T, NA, 10>(a, st, unit_same, al);
-        case 1u << 11: return go_em<T, NA, 11>(a, st, unit_same, al);
-        case 1u << 12: return go_em<T, NA, 12>(a, st, unit_same, al);
-        case 1u << 13:
-            if constexpr (NA * (1u << 13) * es <= kSmemPoolMax)
-                return go_em<T, NA, 13>(a, st, unit_same, al);
-            else
-                return cudaErrorInvalidValue;
-        case 1u << 14:
-            if constexpr (NA * (1u << 14) * es <= kSmemPoolMax)
-                return go_em<T, NA, 14>(a, st, unit_same, al);
-            else
-                return cudaErrorInvalidValue;
-        default: return cudaErrorInvalidValue;
-    }
-}
-
 cudaError_t launch_smem(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
                         cudaStream_t st) {
     const bool unit_same =
         a.op != OP_FILL || (a.unit && (a.out_f32 != 0) == (dtype == WRNG_GPU_F32));
     const bool al = aligned_layout_ok();
     if (dtype == WRNG_GPU_F64)
-        return n_arrays == 2 ? dispatch<double, 2>(a, st, unit_same, al)
-                             : dispatch<double, 4>(a, st, unit_same, al);
-    return n_arrays == 2 ? dispatch<float, 2>(a, st, unit_same, al)
-                         : dispatch<float, 4>(a, st, unit_same, al);
+        return n_arrays == 2 ? smem_dispatch_f64_n2(a, st, unit_same, al)
+                             : smem_dispatch_f64_n4(a, st, unit_same, al);
+    return n_arrays == 2 ? smem_dispatch_f32_n2(a, st, unit_same, al)
+                         : smem_dispatch_f32_n4(a, st, unit_same, al);
 }
 
 }  // namespace wg
