@@ -326,18 +326,23 @@ def main():
         kernel_ms = statistics.mean(step_ms)
         algo_bytes = per_gpu * esize
     achieved = algo_bytes / (kernel_ms / 1e3) / 1e9
-    traffic = None
+    # DRAM traffic per launch: dram__bytes_read + dram__bytes_write of the
+    # committed `ncu --set full` capture (profiles/traffic.json), expressed
+    # per output byte and scaled to this launch.
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as fh:
-                tj = json.load(fh)
-            if cfgname in tj:
-                traffic = tj[cfg_name_key(cfgname)]["bytes_per_output_byte"] * algo_bytes
+                tj = json.load(fh).get(cfgname)
+            if tj:
+                traffic = tj["dram_bytes_per_output_byte"] * algo_bytes
+                traffic_src = tj["source"]
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": algo_bytes,
                 "kernel_ms": kernel_ms}
 
@@ -389,10 +394,6 @@ def main():
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
-
-
-def cfg_name_key(name: str) -> str:
-    return name
 
 
 if __name__ == "__main__":
