@@ -165,6 +165,110 @@ __device__ __forceinline__ void phase_b(uint32_t pool_s, uint32_t (&ixb)[NA],
     });
 }
 
+// ---- packed fp32 path (n = 4, fp32 pools): Blackwell FADD2 / FMUL2 ------
+// add/sub/mul.rn.f32x2 round each lane exactly like the scalar op, so two
+// columns (k, k+1) of a thread are transformed by one instruction.
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2_pack(float a, float b) {
+    f2_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(f2_t v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+    f2_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t f2_sub(f2_t a, f2_t b) {
+    f2_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
+    f2_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+template <int LOGN, int VAR, bool AL>
+__device__ __forceinline__ void phase_b2(uint32_t pool_s, uint32_t (&ixb)[4],
+                                         const uint32_t (&stepb)[4],
+                                         f2_t (&u)[4][SmemShape<float, 4, LOGN>::J / 2]) {
+    using S = SmemShape<float, 4, LOGN>;
+    static_assert(S::J % 2 == 0, "column pairs");
+    sfor<0, (int)S::J / 2>([&](auto kc) {
+        constexpr int kp = decltype(kc)::value;
+        float g[4][2];
+        sfor<0, 2>([&](auto hc) {
+            constexpr int h = decltype(hc)::value;
+            sfor<0, 4>([&](auto mc) {
+                constexpr int m = decltype(mc)::value;
+                const uint32_t a =
+                    AL ? ((ixb[m] & S::MASKB) | pool_s) : ((ixb[m] & S::MASKB) + pool_s);
+                g[m][h] = lds<float, (uint32_t)m * S::ABYTES>(a);
+                ixb[m] += stepb[m];
+            });
+        });
+        const f2_t G0 = f2_pack(g[0][0], g[0][1]), G1 = f2_pack(g[1][0], g[1][1]);
+        const f2_t G2 = f2_pack(g[2][0], g[2][1]), G3 = f2_pack(g[3][0], g[3][1]);
+        if constexpr (VAR == 0) {
+            const f2_t PP = f2_add(G0, G1), Q = f2_sub(G0, G1);
+            const f2_t R = f2_add(G2, G3), Sd = f2_sub(G2, G3);
+            u[0][kp] = f2_add(PP, R);
+            u[1][kp] = f2_add(Q, Sd);
+            u[2][kp] = f2_sub(PP, R);
+            u[3][kp] = f2_sub(Q, Sd);
+        } else {
+            const f2_t T = f2_mul(f2_pack(0.5f, 0.5f), f2_add(f2_add(G0, G1), f2_add(G2, G3)));
+            u[0][kp] = f2_sub(T, G0);
+            u[1][kp] = f2_sub(T, G1);
+            u[2][kp] = f2_sub(T, G2);
+            u[3][kp] = f2_sub(T, G3);
+        }
+    });
+}
+
+template <int LOGN, int EM, int MD>
+__device__ __forceinline__ void phase_c2(const f2_t (&u)[4][SmemShape<float, 4, LOGN>::J / 2],
+                                         float c0, uint32_t pool_s, char* out_p, uint32_t en,
+                                         const EmitCfg& ec, double& withheld_out) {
+    using S = SmemShape<float, 4, LOGN>;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t my_s = pool_s + tid * 4u;
+    float* ob = MD == 1 ? reinterpret_cast<float*>(out_p) + tid : nullptr;
+    const f2_t C = f2_pack(c0, c0), Z = f2_pack(0.0f, 0.0f);
+    sfor<0, (int)S::J / 2>([&](auto kc) {
+        constexpr int kp = decltype(kc)::value;
+        sfor<0, 4>([&](auto mc) {
+            constexpr int m = decltype(mc)::value;
+            const f2_t Y = f2_mul(C, u[m][kp]);
+            float y[2];
+            f2_unpack(Y, y[0], y[1]);
+            float e[2];
+            if constexpr (MD == 1) f2_unpack(f2_add(Y, Z), e[0], e[1]);  // 0 + 1 * v
+            sfor<0, 2>([&](auto hc) {
+                constexpr int h = decltype(hc)::value;
+                constexpr int k = 2 * kp + h;
+                constexpr uint32_t col = m * S::N + k * S::NTH;
+                sts<float, col * 4u>(my_s, y[h]);
+                if constexpr (MD == 1) {
+                    if (!(m == 3 && k == (int)S::J - 1) || tid != S::NTH - 1) ob[col] = e[h];
+                } else if constexpr (MD == 2) {
+                    const uint32_t flat = col + tid;
+                    if (flat < en)
+                        emit_one<float, EM>(out_p, flat, y[h], ec.out_f32, ec.unit, ec.mu,
+                                            ec.sigma);
+                }
+                if (m == 3 && k == (int)S::J - 1 && tid == S::NTH - 1)
+                    withheld_out = (double)y[h];
+            });
+        });
+    });
+}
+
 // Phase C: scale, store in place, emit.  MD 0: no emission; 1: the whole
 // exposed pool (all but the withheld slot) with unit output: unconditional
 // stores at immediate offsets; 2: partial window / generic output.
@@ -273,21 +377,35 @@ __device__ __forceinline__ bool smem_pass(uint32_t pool_s, uint32_t mode, uint32
     if (prefetch && tid < 32)
         draw_pass_params_warp<NA>(&sm_at<uint64_t>(S::TAB_OFF), ctl,
                                   &sm_at<uint64_t>(S::WBUF_OFF), N, slot ^ 1);
-    T u[NA][S::J];
-    if (NA == 2 || variant == 0)
-        phase_b<T, NA, LOGN, 0, AL>(pool_s, ixb, stepb, u);
-    else
-        phase_b<T, NA, LOGN, 1, AL>(pool_s, ixb, stepb, u);
-    __syncthreads();
-
     const T c0 = (T)c0d, c1 = (T)c1d;  // fp32 pools: rounded once (docs/n4_spec.md §4)
     double wh = 0.0;
-    if (emit_n == 0)
-        phase_c<T, NA, LOGN, EM, 0>(u, c0, c1, pool_s, out_p, 0, ec, wh);
-    else if (EM == EM_UNIT && emit_n == (uint32_t)S::CAP)
-        phase_c<T, NA, LOGN, EM, 1>(u, c0, c1, pool_s, out_p, emit_n, ec, wh);
-    else
-        phase_c<T, NA, LOGN, EM, 2>(u, c0, c1, pool_s, out_p, emit_n, ec, wh);
+    if constexpr (sizeof(T) == 4 && NA == 4 && S::J % 2 == 0) {
+        f2_t u[4][S::J / 2];
+        if (variant == 0)
+            phase_b2<LOGN, 0, AL>(pool_s, ixb, stepb, u);
+        else
+            phase_b2<LOGN, 1, AL>(pool_s, ixb, stepb, u);
+        __syncthreads();
+        if (emit_n == 0)
+            phase_c2<LOGN, EM, 0>(u, c0, pool_s, out_p, 0, ec, wh);
+        else if (EM == EM_UNIT && emit_n == (uint32_t)S::CAP)
+            phase_c2<LOGN, EM, 1>(u, c0, pool_s, out_p, emit_n, ec, wh);
+        else
+            phase_c2<LOGN, EM, 2>(u, c0, pool_s, out_p, emit_n, ec, wh);
+    } else {
+        T u[NA][S::J];
+        if (NA == 2 || variant == 0)
+            phase_b<T, NA, LOGN, 0, AL>(pool_s, ixb, stepb, u);
+        else
+            phase_b<T, NA, LOGN, 1, AL>(pool_s, ixb, stepb, u);
+        __syncthreads();
+        if (emit_n == 0)
+            phase_c<T, NA, LOGN, EM, 0>(u, c0, c1, pool_s, out_p, 0, ec, wh);
+        else if (EM == EM_UNIT && emit_n == (uint32_t)S::CAP)
+            phase_c<T, NA, LOGN, EM, 1>(u, c0, c1, pool_s, out_p, emit_n, ec, wh);
+        else
+            phase_c<T, NA, LOGN, EM, 2>(u, c0, c1, pool_s, out_p, emit_n, ec, wh);
+    }
     if (tid == NTH - 1) ctl->withheld = wh;  // wallace.cpp:136
     if (tid == 0) {
         ctl->tracked = target;  // wallace.cpp:135
