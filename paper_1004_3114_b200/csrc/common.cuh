@@ -30,6 +30,11 @@ __device__ __forceinline__ uint32_t nib(uint64_t w, uint32_t m) {
     // next_int_below (uniform.cpp:47-51)
     return (uint32_t)(u53(w) * (double)m);
 }
+// next_int_below(2^k): (w >> 11) * 2^-53 * 2^k is exact, so its floor is the
+// integer w >> (64 - k) — identical to nib(w, 2^k) for 1 <= k <= 20.
+__device__ __forceinline__ uint32_t nib_pow2(uint64_t w, uint32_t log2m) {
+    return (uint32_t)(w >> (64 - log2m));
+}
 __device__ __forceinline__ double chi2_target(double r, uint32_t nu) {
     // wallace.cpp:27-31
     double t = r + sqrt(2.0 * (double)nu - 1.0);
@@ -238,10 +243,11 @@ __device__ __forceinline__ void draw_pass_params_warp(uint64_t* tab, Ctl* ctl, u
     const uint64_t w_next = __shfl_down_sync(0xffffffffu, w, 1);
     LfgParams& p = slot ? ctl->cur2 : ctl->cur;
     if (NA == 2) {
-        if (lane == 0) p.stride[0] = nib(w, 2) == 0 ? 3 : 5;
-        if (lane == 1) p.stride[1] = nib(w, 2) == 0 ? 7 : 11;
-        if (lane == 2) p.offset[0] = nib(w, N);
-        if (lane == 3) p.offset[1] = nib(w, N);
+        const uint32_t lg = (uint32_t)__ffs(N) - 1;
+        if (lane == 0) p.stride[0] = nib_pow2(w, 1) == 0 ? 3 : 5;
+        if (lane == 1) p.stride[1] = nib_pow2(w, 1) == 0 ? 7 : 11;
+        if (lane == 2) p.offset[0] = nib_pow2(w, lg);
+        if (lane == 3) p.offset[1] = nib_pow2(w, lg);
         if (lane == 4) {
             // rotation_from_uniform: t from word 4, region from word 5
             // (wallace.cpp:44-49), rotation_from_t (wallace.cpp:33-42)
@@ -265,11 +271,11 @@ __device__ __forceinline__ void draw_pass_params_warp(uint64_t* tab, Ctl* ctl, u
         // strides from {3,5}, {7,11}, {13,17}, {19,23} (docs/n4_spec.md §2)
         if (lane < 4) {
             const uint32_t lo = lane == 0 ? 3 : lane == 1 ? 7 : lane == 2 ? 13 : 19;
-            p.stride[lane] = nib(w, 2) == 0 ? lo : lo + (lane == 0 ? 2 : 4);
+            p.stride[lane] = nib_pow2(w, 1) == 0 ? lo : lo + (lane == 0 ? 2 : 4);
         } else if (lane < 8) {
-            p.offset[lane - 4] = nib(w, N);
+            p.offset[lane - 4] = nib_pow2(w, (uint32_t)__ffs(N) - 1);
         } else if (lane == 8) {
-            p.variant = nib(w, 2);
+            p.variant = nib_pow2(w, 1);
         } else if (lane == 9) {
             p.c = 0.0;
             p.s = 0.0;

@@ -319,7 +319,7 @@ __device__ __forceinline__ void phase_c(const T (&u)[NA][SmemShape<T, NA, LOGN>:
 // The chi-squared scale (wallace.cpp:59-69) is derived by EVERY thread from
 // the broadcast (tracked, withheld): warp-uniform, so its fp64 div/sqrt
 // chain overlaps the gathers instead of serialising one lane of warp 0.
-template <typename T, int NA, int LOGN, int EM, bool AL>
+template <typename T, int NA, int LOGN, int EM, bool AL, bool COLD>
 __device__ __forceinline__ bool smem_pass(uint32_t pool_s, uint32_t mode, uint32_t emit_n,
                                           char* out_p, const EmitCfg& ec, wrng_gpu_params* rec,
                                           bool prefetch, T* prev, int slot) {
@@ -343,9 +343,13 @@ __device__ __forceinline__ bool smem_pass(uint32_t pool_s, uint32_t mode, uint32
     // regenerate folds the scale into the matrix (wallace.cpp:116-117)
     const double c0d = NA == 2 ? cp.c * scale : (variant ? scale : 0.5 * scale);
     const double c1d = NA == 2 ? cp.s * scale : scale;
-    if (tid == 0) {
-        ctl->error = e;
-        if (!e && rec) {
+    if (e) {  // every thread sees the same e (wallace.cpp:59-61)
+        if (tid == 0) ctl->error = e;
+        __syncthreads();
+        return false;
+    }
+    if (COLD && tid == 0) {
+        if (rec) {
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
                 rec->stride[m] = cp.stride[m];
@@ -358,17 +362,13 @@ __device__ __forceinline__ bool smem_pass(uint32_t pool_s, uint32_t mode, uint32
             rec->scale = scale;
             rec->target_sumsq = target;
         }
-        if (prev && !e) {
+        if (prev) {
             ctl->prev_tracked = tracked;
             ctl->prev_withheld = withheld;
             ctl->have_prev = 1;
         }
     }
-    if (e) {
-        __syncthreads();
-        return false;
-    }
-    if (prev) {
+    if (COLD && prev) {
         // the pre-pass pool becomes the inactive buffer (wallace.cpp:170-174)
         constexpr uint32_t NVEC = (uint32_t)(S::NVALS * sizeof(T) / 16);
         uint4* dst = reinterpret_cast<uint4*>(prev);
@@ -587,9 +587,14 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
             ++pass_i;
             const bool last_launch = pass_i == total_passes;
             const bool prefetch = !last_launch && !(lastp && will_restart);
-            if (!smem_pass<T, NA, LOGN, EM, AL>(pool_s, mode, lastp ? emit_n : 0u, out_p, ec,
-                                                nullptr, prefetch,
-                                                last_launch ? prev_buf() : nullptr, slot)) {
+            const uint32_t en = lastp ? emit_n : 0u;
+            const bool ok =
+                last_launch
+                    ? smem_pass<T, NA, LOGN, EM, AL, true>(pool_s, mode, en, out_p, ec, nullptr,
+                                                           prefetch, prev_buf(), slot)
+                    : smem_pass<T, NA, LOGN, EM, AL, false>(pool_s, mode, en, out_p, ec, nullptr,
+                                                            prefetch, nullptr, slot);
+            if (!ok) {
                 err = ctl->error;
                 break;
             }
@@ -625,7 +630,7 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
             ++pass_i;
             const bool last_launch = pass_i == total_passes;
             wrng_gpu_params* rec = (a.params_out && last_launch) ? a.params_out + p : nullptr;
-            if (!smem_pass<T, NA, LOGN, EM, AL>(pool_s, mode, 0u, nullptr, ec, rec,
+            if (!smem_pass<T, NA, LOGN, EM, AL, true>(pool_s, mode, 0u, nullptr, ec, rec,
                                                 !last_launch,
                                                 last_launch ? prev_buf() : nullptr, slot)) {
                 err = ctl->error;
