@@ -290,6 +290,41 @@ __device__ __forceinline__ void draw_pass_params_warp(uint64_t* tab, Ctl* ctl, u
     __syncwarp();
 }
 
+// Same draw for n = 4, executed branch-free by EVERY warp of the CTA with
+// only `writer` (warp 0) storing: all warps run an identical instruction
+// stream, so the draw's latency does not unbalance the pass barrier.  The
+// uint32 fields stride[0..3], offset[0..3], variant of LfgParams are words
+// 0..8, i.e. lane k writes word k.
+template <int NA>
+__device__ __forceinline__ void draw_pass_params_all(uint64_t* tab, Ctl* ctl, uint32_t N,
+                                                     int slot, bool writer) {
+    if constexpr (NA == 2) {
+        if (writer) draw_pass_params_warp<2>(tab, ctl, nullptr, N, slot);
+    } else {
+        constexpr uint32_t K = PassWords<4>::K;
+        const uint32_t lane = threadIdx.x & 31u;
+        const uint32_t r = ctl->r;
+        uint32_t i = r + lane;
+        i = i >= kTable ? i - kTable : i;
+        uint32_t s = i + kGap;
+        s = s >= kTable ? s - kTable : s;
+        const bool mine = lane < K;
+        const uint64_t w = mine ? tab[i] + tab[s] : 0ull;
+        if (writer && mine) tab[i] = w;
+        const uint32_t lo = lane == 0 ? 3u : lane == 1 ? 7u : lane == 2 ? 13u : 19u;
+        const uint32_t strd = (w >> 63) ? lo + (lane == 0 ? 2u : 4u) : lo;
+        const uint32_t offs = (uint32_t)(w >> (64 - ((uint32_t)__ffs(N) - 1)));
+        const uint32_t val = lane < 4 ? strd : lane < 8 ? offs : (uint32_t)(w >> 63);
+        LfgParams& p = slot ? ctl->cur2 : ctl->cur;
+        if (writer && mine) reinterpret_cast<uint32_t*>(&p)[lane] = val;
+        if (writer && lane == 31) {
+            const uint32_t nr = r + K;
+            ctl->r = nr >= kTable ? nr - kTable : nr;
+            ctl->draws += K;
+        }
+    }
+}
+
 // Sequential sum of squares in Pool::direct_sumsq order (wallace.cpp:13-18).
 template <typename T>
 __device__ double seq_sumsq(const T* v, uint32_t n) {

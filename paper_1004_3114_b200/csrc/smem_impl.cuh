@@ -374,9 +374,8 @@ __device__ __forceinline__ bool smem_pass(uint32_t pool_s, uint32_t mode, uint32
         uint4* dst = reinterpret_cast<uint4*>(prev);
         for (uint32_t i = tid; i < NVEC; i += NTH) dst[i] = sm_at<uint4>(S::POOL_OFF + i * 16);
     }
-    if (prefetch && tid < 32)
-        draw_pass_params_warp<NA>(&sm_at<uint64_t>(S::TAB_OFF), ctl,
-                                  &sm_at<uint64_t>(S::WBUF_OFF), N, slot ^ 1);
+    if (prefetch)
+        draw_pass_params_all<NA>(&sm_at<uint64_t>(S::TAB_OFF), ctl, N, slot ^ 1, tid < 32);
     const T c0 = (T)c0d, c1 = (T)c1d;  // fp32 pools: rounded once (docs/n4_spec.md §4)
     double wh = 0.0;
     if constexpr (sizeof(T) == 4 && NA == 4 && S::J % 2 == 0) {
@@ -487,6 +486,8 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
             ctl->active = 0;
             ctl->error = 0;
             ctl->have_prev = 0;
+            ctl->cur.c = ctl->cur.s = ctl->cur2.c = ctl->cur2.s = 0.0;
+            ctl->cur.pad_ = ctl->cur2.pad_ = 0;
         }
         lfg_seed(tab, ctl, wbuf, a.seed, a.stream0 + p, S::STEP);
     } else {
@@ -503,6 +504,8 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
             ctl->withheld = meta->withheld[act];
             ctl->error = 0;
             ctl->have_prev = 0;
+            ctl->cur.c = ctl->cur.s = ctl->cur2.c = ctl->cur2.s = 0.0;
+            ctl->cur.pad_ = ctl->cur2.pad_ = 0;
         }
         const uint4* src = reinterpret_cast<const uint4*>(static_cast<const T*>(a.buf[act]) +
                                                           (uint64_t)p * NVALS);
