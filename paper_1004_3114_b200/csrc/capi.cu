@@ -64,6 +64,9 @@ struct wrng_gpu {
     size_t stage_bytes = 0;
     cudaEvent_t gen_done[2] = {nullptr, nullptr}, copy_done[2] = {nullptr, nullptr};
     std::vector<Ctr> ctr;
+    void* l2_base = nullptr;
+    uint64_t l2_bytes = 0;
+    float l2_hit = 0.f;
     uint64_t launches = 0;
     std::string err;
 };
@@ -91,6 +94,25 @@ wrng_gpu_status cuda_fail(wrng_gpu* g, cudaError_t e, const char* where) {
         if (e_ != cudaSuccess) return cuda_fail(g, e_, #expr);     \
         ++g->launches;                                             \
     } while (0)
+
+// HBM pools live in transposed storage (hbm_pos); every host boundary
+// (read/write_pool, export/import, host init) sees natural order.
+void permute_pool(const wrng_gpu* g, void* data, bool to_storage) {
+    if (!g->hbm) return;
+    const HbmSplit sp = hbm_split(g->N);
+    if (sp.lc == 0) return;  // one row: identity
+    const size_t es = g->esize;
+    std::vector<char> tmp(g->nvals * es);
+    char* d = static_cast<char*>(data);
+    for (uint64_t i = 0; i < g->nvals; ++i) {
+        const uint64_t pos = hbm_pos(i, g->N, sp);
+        if (to_storage)
+            std::memcpy(tmp.data() + pos * es, d + i * es, es);
+        else
+            std::memcpy(tmp.data() + i * es, d + pos * es, es);
+    }
+    std::memcpy(d, tmp.data(), tmp.size());
+}
 
 // Orders work on stream `s` after everything queued so far on the handle.
 wrng_gpu_status order_on(wrng_gpu* g, cudaStream_t s) {
@@ -120,6 +142,9 @@ KernelArgs base_args(const wrng_gpu* g) {
     a.mu = 0.0;
     a.sigma = 1.0;
     a.unit = 1;
+    a.l2_base = g->l2_base;
+    a.l2_bytes = g->l2_bytes;
+    a.l2_hit = g->l2_hit;
     return a;
 }
 
@@ -276,6 +301,8 @@ wrng_gpu_status run_hbm(wrng_gpu* g, uint32_t p, Ctr c, const std::vector<Ev>& e
                 ps.end_refill = e.end_refill;
                 LAUNCH(launch_hbm_pass(NA, dt, a, g->params, ps, s));
                 c.active ^= 1u;
+                if (e.emit_n)
+                    LAUNCH(launch_hbm_emit_t(NA, dt, a, c.active, e.emit_n, e.out_off, s));
             } else if (e.kind == Ev::DRIFT) {
                 LAUNCH(launch_hbm_drift(NA, dt, a, c.active,
                                         (g->cfg.flags & WRNG_GPU_DRIFT_TREE) != 0, g->scratch,
@@ -283,7 +310,7 @@ wrng_gpu_status run_hbm(wrng_gpu* g, uint32_t p, Ctr c, const std::vector<Ev>& e
             }
         }
         if (jend < ev.size()) {  // RESTART
-            LAUNCH(launch_hbm_init(NA, dt, a, c.active, 0, s));
+            LAUNCH(launch_hbm_init(NA, dt, a, c.active, 0, g->scratch, s));
             ++jend;
         }
         i = jend;
@@ -502,7 +529,8 @@ wrng_gpu_status run_op(wrng_gpu* g, Op op, wrng_gpu_params* params_host) {
                                         (g->cfg.flags & WRNG_GPU_DRIFT_TREE) != 0, g->scratch,
                                         g->stream));
             } else if (op == OP_RESTART) {
-                LAUNCH(launch_hbm_init(g->cfg.n_arrays, g->cfg.dtype, a, c.active, 0, g->stream));
+                LAUNCH(launch_hbm_init(g->cfg.n_arrays, g->cfg.dtype, a, c.active, 0, g->scratch,
+                                       g->stream));
                 c.avail = 0;
             }
         }
@@ -592,6 +620,7 @@ wrng_gpu_status host_init(wrng_gpu* g) {
         meta[p] = PoolMeta{};
         meta[p].tracked[0] = q;
         meta[p].withheld[0] = wx;
+        permute_pool(g, vals.data(), true);
         CK(cudaMemcpy(static_cast<char*>(g->buf[0]) + (size_t)p * vals.size(), vals.data(),
                       vals.size(), cudaMemcpyHostToDevice));
     }
@@ -628,10 +657,25 @@ wrng_gpu_status alloc_handle(const wrng_gpu_config* cfg, wrng_gpu** out) {
     if (cfg->device < 0 || cfg->device >= ndev) return fail(g, WRNG_GPU_ENODEV, "bad device");
     DeviceGuard dg(cfg->device);
     const size_t pool_bytes = (size_t)cfg->pools * g->nvals * g->esize;
-    for (int b = 0; b < 2; ++b) {
-        if (cudaMalloc(&g->buf[b], pool_bytes) != cudaSuccess)
-            return fail(g, WRNG_GPU_ENOMEM, "pool allocation failed");
-        CK(cudaMemset(g->buf[b], 0, pool_bytes));
+    // both buffers in one allocation: one L2 access window covers them
+    if (cudaMalloc(&g->buf[0], 2 * pool_bytes) != cudaSuccess)
+        return fail(g, WRNG_GPU_ENOMEM, "pool allocation failed");
+    g->buf[1] = static_cast<char*>(g->buf[0]) + pool_bytes;
+    CK(cudaMemset(g->buf[0], 0, 2 * pool_bytes));
+    if (g->hbm) {
+        int maxp = 0, maxw = 0;
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, cfg->device);
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, cfg->device);
+        const size_t want = 2 * pool_bytes;
+        if (maxp > 0 && maxw > 0) {
+            size_t cur = 0;
+            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            const size_t setaside = std::min<size_t>(want, (size_t)maxp);
+            if (cur < setaside) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside);
+            g->l2_base = g->buf[0];
+            g->l2_bytes = std::min<size_t>(want, (size_t)maxw);
+            g->l2_hit = (float)std::min(1.0, (double)setaside / (double)g->l2_bytes);
+        }
     }
     CK(cudaMalloc(&g->meta, sizeof(PoolMeta) * cfg->pools));
     CK(cudaMemset(g->meta, 0, sizeof(PoolMeta) * cfg->pools));
@@ -753,7 +797,7 @@ wrng_gpu_status wrng_gpu_create(const wrng_gpu_config* cfg, wrng_gpu_t** out) {
     } else {
         for (uint32_t p = 0; p < cfg->pools && !st; ++p) {
             KernelArgs a = pool_args(g, p);
-            cudaError_t e = launch_hbm_init(cfg->n_arrays, cfg->dtype, a, 0, 1, g->stream);
+            cudaError_t e = launch_hbm_init(cfg->n_arrays, cfg->dtype, a, 0, 1, g->scratch, g->stream);
             st = e == cudaSuccess ? WRNG_GPU_OK : cuda_fail(g, e, "init");
             ++g->launches;
         }
@@ -776,8 +820,8 @@ void wrng_gpu_destroy(wrng_gpu_t* g) {
             DeviceGuard dg(g->cfg.device);
             if (g->stream) cudaStreamSynchronize(g->stream);
             if (g->copy_stream) cudaStreamSynchronize(g->copy_stream);
+            if (g->buf[0]) cudaFree(g->buf[0]);  // both buffers (one allocation)
             for (int b = 0; b < 2; ++b) {
-                if (g->buf[b]) cudaFree(g->buf[b]);
                 if (g->stage[b]) cudaFree(g->stage[b]);
                 if (g->gen_done[b]) cudaEventDestroy(g->gen_done[b]);
                 if (g->copy_done[b]) cudaEventDestroy(g->copy_done[b]);
@@ -863,6 +907,7 @@ wrng_gpu_status wrng_gpu_read_pool(wrng_gpu_t* g, uint32_t pool, double* values,
         std::vector<char> raw(g->nvals * g->esize);
         CK(cudaMemcpy(raw.data(), static_cast<char*>(g->buf[act]) + (size_t)pool * raw.size(),
                       raw.size(), cudaMemcpyDeviceToHost));
+        permute_pool(g, raw.data(), false);
         for (uint64_t i = 0; i < g->nvals; ++i)
             values[i] = g->esize == 8 ? reinterpret_cast<double*>(raw.data())[i]
                                       : (double)reinterpret_cast<float*>(raw.data())[i];
@@ -889,6 +934,7 @@ wrng_gpu_status wrng_gpu_write_pool(wrng_gpu_t* g, uint32_t pool, const double* 
             else
                 reinterpret_cast<float*>(raw.data())[i] = (float)values[i];
         }
+        permute_pool(g, raw.data(), true);
         CK(cudaMemcpy(static_cast<char*>(g->buf[act]) + (size_t)pool * raw.size(), raw.data(),
                       raw.size(), cudaMemcpyHostToDevice));
     }
@@ -929,6 +975,7 @@ wrng_gpu_status wrng_gpu_export_state(wrng_gpu_t* g, uint8_t* buf, size_t cap, s
     for (int b = 0; b < 2; ++b) {
         vals[b].resize(pbytes * P);
         CK(cudaMemcpy(vals[b].data(), g->buf[b], vals[b].size(), cudaMemcpyDeviceToHost));
+        for (uint32_t p = 0; p < P; ++p) permute_pool(g, vals[b].data() + p * pbytes, false);
     }
     const bool v1 = g->cfg.n_arrays == 2 && g->cfg.dtype == WRNG_GPU_F64 && P == 1;
     Writer w;
@@ -1072,6 +1119,8 @@ wrng_gpu_status wrng_gpu_import_state(const uint8_t* bytes, size_t size, int32_t
     DeviceGuard dg(device);
     g->ctr = ctr;
     for (int b = 0; b < 2; ++b) {
+        for (uint32_t p = 0; p < P; ++p)
+            permute_pool(g, vals[b].data() + (size_t)p * nvals * esz, true);
         cudaError_t e = cudaMemcpy(g->buf[b], vals[b].data(), vals[b].size(),
                                    cudaMemcpyHostToDevice);
         if (e != cudaSuccess) {

@@ -411,14 +411,24 @@ __device__ __forceinline__ SumSeg seg_compose(const SumSeg& a, const SumSeg& b) 
     return c;
 }
 
-// Applies a chunk to the exact running sum q; false when it cannot (q not in
-// the chunk's binade, an invalid term, or the binade would be left).
+// After all compositions: store the two increments as the bit patterns of
+// doubles (exact below 2^53; anything larger can only fail to apply), so the
+// serial walk below needs no int <-> double conversion.
+__device__ __forceinline__ void seg_finalize(SumSeg& g) {
+    g.s[0] = __double_as_longlong((double)g.s[0]);
+    g.s[1] = __double_as_longlong((double)g.s[1]);
+}
+
+// Applies a finalized chunk to the exact running sum q; false when it cannot
+// (q not in the chunk's binade, an invalid term, or the binade would be left).
+// Q = q / u is an integer-valued double in [2^52, 2^53): its parity is the
+// lowest mantissa bit and Q + K is exact while below 2^53.
 __device__ __forceinline__ bool seg_apply(double& q, const SumSeg& g) {
     if (!g.valid || !(q > 0.0) || exp2_of(q) != g.e) return false;
-    const long long Q = (long long)(q * pow2d(52 - g.e));  // exact integer < 2^53
-    const long long Qn = Q + g.s[Q & 1];
-    if (Qn >= (1ll << 53)) return false;
-    q = (double)Qn * pow2d(g.e - 52);  // exact
+    const double Q = q * pow2d(52 - g.e);
+    const double Qn = Q + __longlong_as_double(g.s[__double_as_longlong(Q) & 1]);
+    if (!(Qn < 0x1.0p53)) return false;
+    q = Qn * pow2d(g.e - 52);
     return true;
 }
 
@@ -465,7 +475,10 @@ __device__ double exact_sumsq_cta(const T* v, uint32_t n, void* scratch) {
         g.valid = 0;
     }
     __syncthreads();
-    if (t < nch) seg[t] = g;
+    if (t < nch) {
+        seg_finalize(g);
+        seg[t] = g;
+    }
     __syncthreads();
     // walk (one thread): O(1) per chunk, term by term only where needed
     double q = 0.0;

@@ -1,17 +1,30 @@
 // HBM engine: pools too large for shared memory (BASELINE.json config C2,
-// one 4 x 2^20 fp64 pool).  Double-buffered in global memory (the 2 x 32 MiB
-// of C2 stay L2-resident on the 126 MB L2), one grid-wide launch per pass,
-// host-driven control flow (capi.cu plan_fill) mirroring wallace.cpp:169-216.
+// one 4 x 2^20 fp64 pool).  Double-buffered in global memory, one grid-wide
+// launch per pass, host-driven control flow (capi.cu plan_fill) mirroring
+// wallace.cpp:169-216.
+//
+// Transposed storage.  Each array of N = C * R values (R = min(512, N)) is
+// stored as C rows of R: value i lives at (i mod C) * R + i / C
+// (hbm_pos, internal.h).  For output columns j = j_hi * C + j_lo with a fixed
+// j_lo, the sources (a j + g) mod N of one array all lie in ONE stored row,
+// (a j_lo + g) mod C, at positions (a j_hi + (a j_lo + g) / C) mod R.  So a
+// CTA owning a few output rows j_lo loads whole source rows with coalesced
+// loads, gathers from shared memory with an odd stride (conflict-free), and
+// writes its output rows with coalesced stores; the natural-order output
+// stream gets JLO consecutive values per thread and array.  Every gathered
+// byte is used, instead of one 8-byte value per 32-byte sector of a direct
+// strided gather.
+#include <utility>
+
 #include "common.cuh"
 
 namespace wg {
 
 // ---------------------------------------------------------------------------
+// pass parameters: one warp draws the uniform-generator part of `npass`
+// consecutive passes; the scale needs the previous pass's withheld value and
+// is derived inside each pass kernel.
 // ---------------------------------------------------------------------------
-
-// One warp per pool: the LFG-dependent part of `npass` consecutive passes'
-// parameters (strides, offsets, variant / rotation).  The scale needs the
-// previous pass's withheld value and is derived inside each pass kernel.
 template <int NA>
 __global__ void k_hbm_params(uint32_t N, LfgState* lfg, wrng_gpu_params* params,
                              uint32_t npass, PoolMeta* meta) {
@@ -41,8 +54,8 @@ __global__ void k_hbm_params(uint32_t N, LfgState* lfg, wrng_gpu_params* params,
             p.pad_ = 0;
             p.c = lp.c;
             p.s = lp.s;
-            p.scale = 0.0;         // derived in the pass kernel from the
-            p.target_sumsq = 0.0;  // previous pass's withheld value
+            p.scale = 0.0;
+            p.target_sumsq = 0.0;
             params[(uint64_t)blockIdx.x * npass + ps] = p;
         }
         __syncwarp();
@@ -64,113 +77,125 @@ cudaError_t launch_hbm_params(uint32_t n_arrays, uint32_t N, LfgState* lfg,
     return cudaGetLastError();
 }
 
-constexpr uint32_t kHbmThreads = 256;
-constexpr uint32_t kHbmJ = 4;
+// ---------------------------------------------------------------------------
+// one regeneration pass (wallace.cpp:113-137) on transposed storage
+// ---------------------------------------------------------------------------
+constexpr uint32_t kJlo = 4;  // output rows per CTA
 
-template <typename T, int NA>
-__global__ void __launch_bounds__(kHbmThreads) k_hbm_pass(KernelArgs a,
-                                                          wrng_gpu_params* params,
-                                                          HbmPass ps) {
+// Output element with an evict-first (streaming) store, so the write-once
+// output stream does not push the pool buffers out of L2.
+template <typename T>
+__device__ __forceinline__ void put_out_cs(void* out, uint64_t i, T v, uint32_t out_f32,
+                                           uint32_t unit, double mu, double sigma) {
+    double o = unit ? (double)v + 0.0 : mu + sigma * (double)v;
+    if (unit && out_f32) {
+        __stcs(static_cast<float*>(out) + i, (float)v + 0.0f);
+        return;
+    }
+    if (out_f32)
+        __stcs(static_cast<float*>(out) + i, (float)o);
+    else
+        __stcs(static_cast<double*>(out) + i, o);
+}
+
+template <typename T, int NA, int JL>
+__global__ void __launch_bounds__(512, 3) k_hbm_pass(KernelArgs a, wrng_gpu_params* params,
+                                                  HbmPass ps) {
+    extern __shared__ __align__(16) unsigned char hsm[];
+    T* rows = reinterpret_cast<T*>(hsm);  // [NA][R]
     __shared__ double s_c0, s_c1, s_target, s_scale;
     __shared__ int s_err;
-    const uint32_t N = a.N, mask = N - 1;
+    const uint32_t N = a.N;
+    const HbmSplit sp = hbm_split(N);
+    const uint32_t R = 1u << sp.lr, C = 1u << sp.lc;
     PoolMeta* meta = a.meta;
     const uint32_t src = ps.src, dst = src ^ 1u;
     const wrng_gpu_params prm = params[ps.param_idx];
-    if (threadIdx.x == 0) {
+    const uint32_t t = threadIdx.x;
+    const T* spool = static_cast<const T*>(a.buf[src]);
+    T* dpool = static_cast<T*>(a.buf[dst]);
+    const uint32_t jlo0 = blockIdx.x * JL;
+
+    // software pipeline: sources of row r + 1 load while row r computes
+    T nxt[NA];
+    uint32_t shift[JL][NA];
+#pragma unroll
+    for (int r = 0; r < JL; ++r)
+#pragma unroll
+        for (int m = 0; m < NA; ++m)
+            shift[r][m] = ((prm.stride[m] * (jlo0 + r) + prm.offset[m]) >> sp.lc) & (R - 1);
+    auto load_row = [&](int r) {
+#pragma unroll
+        for (int m = 0; m < NA; ++m) {
+            const uint32_t srow = (prm.stride[m] * (jlo0 + r) + prm.offset[m]) & (C - 1);
+            nxt[m] = __ldg(spool + (uint64_t)m * N + (uint64_t)srow * R + t);
+        }
+    };
+    load_row(0);
+    if (t == 0) {
         int err = meta->error ? -1 : 0;
-        double tracked = meta->tracked[src], withheld = meta->withheld[src];
+        const double tracked = meta->tracked[src], withheld = meta->withheld[src];
         if (!err) {
-            if (!(tracked > 0.0)) {
-                err = WRNG_GPU_ECORRUPT;
-            } else {
-                double target, scale;
-                if (a.mode == WRNG_GPU_CHISQ) {
-                    target = chi2_target(withheld, NA * N);
-                    scale = sqrt(target / tracked);
-                } else {
-                    scale = 1.0;
-                    target = tracked;
-                }
+            double scale, target;
+            err = pass_scale(tracked, withheld, NA * N, a.mode, scale, target);
+            if (!err) {
                 s_target = target;
                 s_scale = scale;
-                if (NA == 2) {
-                    s_c0 = prm.c * scale;
-                    s_c1 = prm.s * scale;
-                } else {
-                    s_c0 = 0.5 * scale;
-                    s_c1 = scale;
-                }
+                // regenerate folds the scale into the matrix (wallace.cpp:116-117)
+                s_c0 = NA == 2 ? prm.c * scale : (prm.variant ? scale : 0.5 * scale);
+                s_c1 = NA == 2 ? prm.s * scale : scale;
             }
         }
         s_err = err;
     }
     __syncthreads();
     if (s_err) {
-        if (s_err > 0 && blockIdx.x == 0 && threadIdx.x == 0) meta->error = s_err;
+        if (s_err > 0 && blockIdx.x == 0 && t == 0) meta->error = s_err;
         return;
     }
-    const T* sp = static_cast<const T*>(a.buf[src]);
-    T* dp = static_cast<T*>(a.buf[dst]);
-    T c0, c1;
-    if (sizeof(T) == 4) {
-        c0 = (T)(float)s_c0;
-        c1 = (T)(float)s_c1;
-    } else {
-        c0 = (T)s_c0;
-        c1 = (T)s_c1;
-    }
-    uint32_t stv[NA], ofv[NA];
+    const T c0 = (T)s_c0, c1 = (T)s_c1;  // fp32 pools: rounded once
+    const uint32_t variant = prm.variant;
 #pragma unroll
-    for (int m = 0; m < NA; ++m) {
-        stv[m] = prm.stride[m];
-        ofv[m] = prm.offset[m];
-    }
-    const uint32_t nth = blockDim.x;
-    const uint32_t j0 = blockIdx.x * (nth * kHbmJ) + threadIdx.x;
-    T v[NA][kHbmJ];
+    for (int r = 0; r < JL; ++r) {
+        const uint32_t jlo = jlo0 + r;
 #pragma unroll
-    for (int k = 0; k < (int)kHbmJ; ++k) {
-        const uint32_t j = j0 + k * nth;
+        for (int m = 0; m < NA; ++m) rows[m * R + t] = nxt[m];
+        __syncthreads();
+        if (r + 1 < JL) load_row(r + 1);
+        T g[NA];
 #pragma unroll
         for (int m = 0; m < NA; ++m)
-            v[m][k] = __ldg(sp + (uint64_t)m * N + ((stv[m] * j + ofv[m]) & mask));
-    }
-    char* outc = static_cast<char*>(a.out) + ps.out_off * (a.out_f32 ? 4 : 8);
-#pragma unroll
-    for (int k = 0; k < (int)kHbmJ; ++k) {
-        const uint32_t j = j0 + k * nth;
+            g[m] = rows[m * R + ((prm.stride[m] * t + shift[r][m]) & (R - 1))];
         T y[NA];
         if (NA == 2) {
-            T xs = v[0][k], ys = v[1][k];
-            y[0] = c0 * xs + c1 * ys;
-            y[1] = c0 * ys - c1 * xs;
+            y[0] = c0 * g[0] + c1 * g[NA > 1 ? 1 : 0];
+            y[NA > 1 ? 1 : 0] = c0 * g[NA > 1 ? 1 : 0] - c1 * g[0];
         } else {
-            T a0 = v[0][k], a1 = v[NA > 1 ? 1 : 0][k], a2 = v[NA > 2 ? 2 : 0][k],
-              a3 = v[NA > 3 ? 3 : 0][k];
-            if (prm.variant == 0) {
-                T pp = a0 + a1, q = a0 - a1, r = a2 + a3, s = a2 - a3;
-                y[0] = c0 * (pp + r);
+            const T a0 = g[0], a1 = g[NA > 1 ? 1 : 0], a2 = g[NA > 2 ? 2 : 0],
+                    a3 = g[NA > 3 ? 3 : 0];
+            if (variant == 0) {
+                const T pp = a0 + a1, q = a0 - a1, rr = a2 + a3, s = a2 - a3;
+                y[0] = c0 * (pp + rr);
                 y[NA > 1 ? 1 : 0] = c0 * (q + s);
-                y[NA > 2 ? 2 : 0] = c0 * (pp - r);
+                y[NA > 2 ? 2 : 0] = c0 * (pp - rr);
                 y[NA > 3 ? 3 : 0] = c0 * (q - s);
             } else {
-                T t = (T)0.5 * ((a0 + a1) + (a2 + a3));
-                y[0] = c1 * (t - a0);
-                y[NA > 1 ? 1 : 0] = c1 * (t - a1);
-                y[NA > 2 ? 2 : 0] = c1 * (t - a2);
-                y[NA > 3 ? 3 : 0] = c1 * (t - a3);
+                const T tt = (T)0.5 * ((a0 + a1) + (a2 + a3));
+                y[0] = c0 * (tt - a0);
+                y[NA > 1 ? 1 : 0] = c0 * (tt - a1);
+                y[NA > 2 ? 2 : 0] = c0 * (tt - a2);
+                y[NA > 3 ? 3 : 0] = c0 * (tt - a3);
             }
         }
 #pragma unroll
         for (int m = 0; m < NA; ++m) {
-            dp[(uint64_t)m * N + j] = y[m];
-            const uint64_t flat = (uint64_t)m * N + j;
-            if (flat < ps.emit_n) put_out(outc, flat, y[m], a.out_f32, a.unit, a.mu, a.sigma);
+            dpool[(uint64_t)m * N + (uint64_t)jlo * R + t] = y[m];  // row jlo, coalesced
         }
-        if (j == N - 1) meta->withheld[dst] = (double)y[NA - 1];
+        if (jlo == C - 1 && t == R - 1) meta->withheld[dst] = (double)y[NA - 1];
+        __syncthreads();
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // the exposed window is streamed by k_hbm_emit_t (coalesced transpose)
+    if (blockIdx.x == 0 && t == 0) {
         params[ps.param_idx].scale = s_scale;
         params[ps.param_idx].target_sumsq = s_target;
         meta->tracked[dst] = s_target;
@@ -180,40 +205,128 @@ __global__ void __launch_bounds__(kHbmThreads) k_hbm_pass(KernelArgs a,
     }
 }
 
+// Launch with the handle's persisting-L2 window (pool buffers), if any.
+template <typename... KP, typename... Args>
+static cudaError_t launch_l2(void (*kern)(KP...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t st, const KernelArgs& a, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    cfg.numAttrs = 0;
+    if (a.l2_bytes) {
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow.base_ptr = a.l2_base;
+        attr[0].val.accessPolicyWindow.num_bytes = a.l2_bytes;
+        attr[0].val.accessPolicyWindow.hitRatio = a.l2_hit;
+        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+template <typename T, int NA>
+static void hbm_pass_go(const KernelArgs& a, wrng_gpu_params* params, const HbmPass& ps,
+                        uint32_t R, uint32_t C, size_t smem, cudaStream_t st) {
+    if (C >= kJlo)
+        launch_l2(k_hbm_pass<T, NA, kJlo>, dim3(C / kJlo), dim3(R), smem, st, a, a, params, ps);
+    else if (C == 2)
+        launch_l2(k_hbm_pass<T, NA, 2>, dim3(1), dim3(R), smem, st, a, a, params, ps);
+    else
+        launch_l2(k_hbm_pass<T, NA, 1>, dim3(1), dim3(R), smem, st, a, a, params, ps);
+}
+
 cudaError_t launch_hbm_pass(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
-                            wrng_gpu_params* params, const HbmPass& ps,
-                            cudaStream_t st) {
-    const uint32_t nth = a.N / kHbmJ < kHbmThreads ? a.N / kHbmJ : kHbmThreads;
-    const uint32_t grid = a.N / (nth * kHbmJ);
+                            wrng_gpu_params* params, const HbmPass& ps, cudaStream_t st) {
+    const HbmSplit sp = hbm_split(a.N);
+    const uint32_t R = 1u << sp.lr, C = 1u << sp.lc;
+    const size_t smem = (size_t)n_arrays * R * (dtype == WRNG_GPU_F64 ? 8 : 4);
     if (dtype == WRNG_GPU_F64) {
         if (n_arrays == 2)
-            k_hbm_pass<double, 2><<<grid, nth, 0, st>>>(a, params, ps);
+            hbm_pass_go<double, 2>(a, params, ps, R, C, smem, st);
         else
-            k_hbm_pass<double, 4><<<grid, nth, 0, st>>>(a, params, ps);
+            hbm_pass_go<double, 4>(a, params, ps, R, C, smem, st);
     } else {
         if (n_arrays == 2)
-            k_hbm_pass<float, 2><<<grid, nth, 0, st>>>(a, params, ps);
+            hbm_pass_go<float, 2>(a, params, ps, R, C, smem, st);
         else
-            k_hbm_pass<float, 4><<<grid, nth, 0, st>>>(a, params, ps);
+            hbm_pass_go<float, 4>(a, params, ps, R, C, smem, st);
     }
     return cudaGetLastError();
 }
 
+// Exposed window of a freshly regenerated pool (wallace.cpp:206-213):
+// natural index m*N + j_hi*C + j_lo is stored at m*N + j_lo*R + j_hi, i.e.
+// a (C x R) -> (R x C) transpose per array, done in 32 x 32 shared-memory
+// tiles so both the pool reads and the output writes are coalesced; output
+// stores are evict-first.  Flat indices >= emit_n are not written.
+template <typename T>
+__global__ void __launch_bounds__(256) k_hbm_emit_t(KernelArgs a, uint32_t buf,
+                                                    uint64_t emit_n, uint64_t out_off) {
+    constexpr uint32_t TS = 64;  // 64 x 64 tile, 16 loads + 16 stores per thread
+    __shared__ T tile[TS][TS + 1];
+    if (a.meta->error) return;
+    const uint32_t N = a.N;
+    const HbmSplit sp = hbm_split(N);
+    const uint32_t R = 1u << sp.lr, C = 1u << sp.lc;
+    const T* pool = static_cast<const T*>(a.buf[buf]) + (uint64_t)blockIdx.z * N;
+    const uint32_t jh0 = blockIdx.x * TS, jl0 = blockIdx.y * TS;
+    const uint32_t tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+#pragma unroll
+    for (uint32_t k = 0; k < TS; k += 8) {
+        const uint32_t jl = jl0 + ty + k;  // stored row
+        if (jl < C) {
+            tile[ty + k][tx] = pool[(uint64_t)jl * R + jh0 + tx];
+            tile[ty + k][tx + 32] = pool[(uint64_t)jl * R + jh0 + tx + 32];
+        }
+    }
+    __syncthreads();
+    char* outc = static_cast<char*>(a.out) + out_off * (a.out_f32 ? 4 : 8);
+    const uint64_t mbase = (uint64_t)blockIdx.z * N;
+#pragma unroll
+    for (uint32_t k = 0; k < TS; k += 8) {
+        const uint32_t jh = jh0 + ty + k;
+#pragma unroll
+        for (uint32_t h = 0; h < TS; h += 32) {
+            const uint32_t jl = jl0 + tx + h;
+            const uint64_t flat = mbase + (uint64_t)jh * C + jl;
+            if (jl < C && flat < emit_n)
+                put_out_cs(outc, flat, tile[tx + h][ty + k], a.out_f32, a.unit, a.mu, a.sigma);
+        }
+    }
+}
+
+cudaError_t launch_hbm_emit_t(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
+                              uint32_t buf, uint64_t emit_n, uint64_t out_off, cudaStream_t st) {
+    const HbmSplit sp = hbm_split(a.N);
+    const uint32_t R = 1u << sp.lr, C = 1u << sp.lc;
+    const dim3 grid(R / 64, (C + 63) / 64, n_arrays), block(32, 8);
+    if (dtype == WRNG_GPU_F64)
+        return launch_l2(k_hbm_emit_t<double>, grid, block, 0, st, a, a, buf, emit_n, out_off);
+    return launch_l2(k_hbm_emit_t<float>, grid, block, 0, st, a, a, buf, emit_n, out_off);
+    return cudaGetLastError();
+}
+
+// leftover emission of the live pool: flat [pos, pos + take)
 template <typename T>
 __global__ void k_hbm_emit(KernelArgs a, uint32_t buf, uint64_t pos, uint64_t take,
                            uint64_t out_off) {
     if (a.meta->error) return;
-    const T* sp = static_cast<const T*>(a.buf[buf]) + pos;
+    const T* pool = static_cast<const T*>(a.buf[buf]);
+    const HbmSplit sp = hbm_split(a.N);
     char* o = static_cast<char*>(a.out) + out_off * (a.out_f32 ? 4 : 8);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < take;
          i += (uint64_t)gridDim.x * blockDim.x)
-        put_out(o, i, sp[i], a.out_f32, a.unit, a.mu, a.sigma);
+        put_out(o, i, pool[hbm_pos(pos + i, a.N, sp)], a.out_f32, a.unit, a.mu, a.sigma);
     if (blockIdx.x == 0 && threadIdx.x == 0) a.meta->avail -= take;
 }
 
 cudaError_t launch_hbm_emit(uint32_t, uint32_t dtype, const KernelArgs& a, uint32_t buf,
-                            uint64_t pos, uint64_t take, uint64_t out_off,
-                            cudaStream_t st) {
+                            uint64_t pos, uint64_t take, uint64_t out_off, cudaStream_t st) {
     uint32_t grid = (uint32_t)umin64((take + 255) / 256, 148 * 8);
     if (grid == 0) grid = 1;
     if (dtype == WRNG_GPU_F64)
@@ -223,70 +336,89 @@ cudaError_t launch_hbm_emit(uint32_t, uint32_t dtype, const KernelArgs& a, uint3
     return cudaGetLastError();
 }
 
-// drift_check on an HBM pool (wallace.cpp:225-234).  Default: the exact
-// value of the left-to-right Pool::direct_sumsq (wallace.cpp:13-18) through
-// the binade segment functions of common.cuh, in four launches:
-//   1 chunk sums (approximate)   2 exclusive scan -> binade guess per chunk
-//   3 segment function per chunk, composed per block of 32 chunks
-//   4 one thread walks blocks, then chunks, then terms where needed.
-// tree != 0: blocked parallel reduction instead (documented deviation,
-// relative error ~1e-16 * log n).
+// ---------------------------------------------------------------------------
+// drift_check / init tracked sum on an HBM pool (wallace.cpp:225-234).
+// Default: the exact value of the left-to-right Pool::direct_sumsq
+// (wallace.cpp:13-18) through the binade segment functions of common.cuh:
+//   1 k_sum_chunks: approximate chunk sums, CTA-local exclusive scan, CTA sums;
+//   2 k_sum_segs:   binade guess per chunk from that prefix, segment function
+//                   per chunk, composed per block of 32 chunks;
+//   3 k_sum_walk:   one CTA composes 32-block super-blocks in shared memory;
+//                   thread 0 walks super-blocks, descending into blocks and
+//                   (with the CTA staging data) chunks and terms only where a
+//                   function cannot be applied (~log2 n places).
+// tree != 0: blocked parallel reduction (documented deviation, relative
+// error ~1e-16 * log n).
+// ---------------------------------------------------------------------------
 constexpr uint32_t kSumChunk = 128;
+constexpr uint32_t kSumCta = 256;  // chunks per CTA of kernels 1-2
 
 template <typename T>
-__global__ void k_sum_chunks(KernelArgs a, uint32_t buf, uint64_t nvals, double* approx,
-                             uint32_t nch) {
-    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= nch || a.meta->error) return;
-    const T* v = static_cast<const T*>(a.buf[buf]);
-    const uint64_t lo = (uint64_t)c * kSumChunk, hi = umin64(lo + kSumChunk, nvals);
-    double s = 0.0;
-    for (uint64_t i = lo; i < hi; ++i) s += sq_term(v[i]);
-    approx[c] = s;
+__device__ __forceinline__ double pool_term(const T* v, uint64_t i, uint32_t N,
+                                            const HbmSplit& sp) {
+    return sq_term(v[hbm_pos(i, N, sp)]);
 }
 
-__global__ void __launch_bounds__(1024) k_sum_scan(const double* approx, uint32_t nch,
-                                                   int* e_out, double* pref_scratch) {
-    // approximate exclusive prefix: per-thread serial runs + one block scan
-    __shared__ double part[1024];
-    const uint32_t t = threadIdx.x, per = (nch + 1023) / 1024;
-    const uint32_t lo = t * per, hi = lo + per < nch ? lo + per : nch;
+template <typename T>
+__global__ void __launch_bounds__(kSumCta) k_sum_chunks(KernelArgs a, uint32_t buf,
+                                                        uint64_t nvals, double* pre_local,
+                                                        double* cta_sum, uint32_t nch) {
+    __shared__ double part[kSumCta];
+    const uint32_t t = threadIdx.x, c = blockIdx.x * kSumCta + t;
+    const T* v = static_cast<const T*>(a.buf[buf]);
+    const HbmSplit sp = hbm_split(a.N);
     double s = 0.0;
-    for (uint32_t i = lo; i < hi; ++i) s += approx[i];
+    if (c < nch) {
+        const uint64_t lo = (uint64_t)c * kSumChunk, hi = umin64(lo + kSumChunk, nvals);
+        for (uint64_t i = lo; i < hi; ++i) s += pool_term(v, i, a.N, sp);
+    }
     part[t] = s;
     __syncthreads();
-    for (uint32_t off = 1; off < 1024; off <<= 1) {
-        double x = t >= off ? part[t - off] : 0.0;
+    for (uint32_t off = 1; off < kSumCta; off <<= 1) {  // inclusive scan (approximate)
+        const double x = t >= off ? part[t - off] : 0.0;
         __syncthreads();
         part[t] += x;
         __syncthreads();
     }
-    double pre = t ? part[t - 1] : 0.0;
-    for (uint32_t i = lo; i < hi; ++i) {
-        pref_scratch[i] = pre;
-        e_out[i] = pre > 0.0 ? exp2_of(pre) : -2000;
-        pre += approx[i];
-    }
+    if (c < nch) pre_local[c] = part[t] - s;
+    if (t == kSumCta - 1) cta_sum[blockIdx.x] = part[t];
 }
 
 template <typename T>
-__global__ void k_sum_segs(KernelArgs a, uint32_t buf, uint64_t nvals, const int* e_in,
-                           SumSeg* segs, SumSeg* blocks, uint32_t nch) {
-    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kSumCta) k_sum_segs(KernelArgs a, uint32_t buf, uint64_t nvals,
+                                                      const double* pre_local,
+                                                      const double* cta_sum, SumSeg* segs,
+                                                      SumSeg* blocks, uint32_t nch) {
+    __shared__ double s_base;
+    const uint32_t t = threadIdx.x, c = blockIdx.x * kSumCta + t;
+    if (t < 32) {  // prefix of the previous CTAs' sums (approximate)
+        double x = 0.0;
+        for (uint32_t b = t; b < blockIdx.x; b += 32) x += cta_sum[b];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        if (t == 0) s_base = x;
+    }
+    __syncthreads();
     const T* v = static_cast<const T*>(a.buf[buf]);
+    const HbmSplit sp = hbm_split(a.N);
+    const double pre = c < nch ? s_base + pre_local[c] : 0.0;
+    const int e = pre > 0.0 ? exp2_of(pre) : -2000;
     SumSeg g;
-    const int e = c < nch ? e_in[c] : -2000;
     seg_init(g, e);
     if (c < nch && e > -1000) {
         const double sc = pow2d(52 - e);
         const uint64_t lo = (uint64_t)c * kSumChunk, hi = umin64(lo + kSumChunk, nvals);
-        for (uint64_t i = lo; i < hi; ++i) seg_push(g, sq_term(v[i]), sc);
+        for (uint64_t i = lo; i < hi; ++i) seg_push(g, pool_term(v, i, a.N, sp), sc);
     } else {
         g.valid = 0;
     }
-    if (c < nch) segs[c] = g;
+    if (c < nch) {
+        SumSeg f = g;
+        seg_finalize(f);
+        segs[c] = f;
+    }
     // compose 32 consecutive chunks (lane order) into one block function
-    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t lane = t & 31u;
     for (uint32_t off = 1; off < 32; off <<= 1) {
         SumSeg o;
         o.s[0] = __shfl_down_sync(0xffffffffu, g.s[0], off);
@@ -297,36 +429,95 @@ __global__ void k_sum_segs(KernelArgs a, uint32_t buf, uint64_t nvals, const int
         o.e = __shfl_down_sync(0xffffffffu, g.e, off);
         if ((lane & (2 * off - 1)) == 0) g = seg_compose(g, o);
     }
-    if (lane == 0 && c < nch) blocks[c / 32] = g;
+    if (lane == 0 && c < nch) {
+        if (c + 32 > nch) g.valid = 0;  // partial block
+        blocks[c / 32] = g;             // not finalized: composed again
+    }
 }
 
+constexpr uint32_t kWalkThreads = 256;
+constexpr uint32_t kBlockTerms = 32 * kSumChunk;
+
+// mode 0: drift_check (compare, adopt or flag ECORRUPT); mode 1: set tracked.
 template <typename T>
-__global__ void k_sum_walk(KernelArgs a, uint32_t buf, uint64_t nvals, const SumSeg* segs,
-                           const SumSeg* blocks, uint32_t nch) {
-    if (threadIdx.x != 0 || a.meta->error) return;
+__global__ void __launch_bounds__(kWalkThreads) k_sum_walk(KernelArgs a, uint32_t buf,
+                                                           uint64_t nvals, const SumSeg* segs,
+                                                           const SumSeg* blocks, uint32_t nch,
+                                                           int mode) {
+    extern __shared__ __align__(16) unsigned char wsm[];
+    const uint32_t nblk = (nch + 31) / 32, nsup = (nblk + 31) / 32;
+    SumSeg* sblk = reinterpret_cast<SumSeg*>(wsm);         // [nblk]
+    SumSeg* ssup = sblk + nblk;                             // [nsup]
+    SumSeg* schk = ssup + nsup;                             // [32]
+    double* sterm = reinterpret_cast<double*>(schk + 32);   // [32 * 128]
+    __shared__ uint32_t s_fail;
+    __shared__ double s_q;
+    if (a.meta->error) return;
+    const uint32_t t = threadIdx.x;
+    for (uint32_t b = t; b < nblk; b += kWalkThreads) sblk[b] = blocks[b];
+    __syncthreads();
+    for (uint32_t u = t; u < nsup; u += kWalkThreads) {  // super-blocks of 32 blocks
+        SumSeg g = sblk[u * 32];
+        const uint32_t end = u * 32 + 32 < nblk ? u * 32 + 32 : nblk;
+        for (uint32_t b = u * 32 + 1; b < end; ++b) g = seg_compose(g, sblk[b]);
+        if (u * 32 + 32 > nblk) g.valid = 0;
+        seg_finalize(g);
+        ssup[u] = g;
+    }
+    __syncthreads();
+    for (uint32_t b = t; b < nblk; b += kWalkThreads) seg_finalize(sblk[b]);
     const T* v = static_cast<const T*>(a.buf[buf]);
-    double q = 0.0;
-    const uint32_t nblk = (nch + 31) / 32;
-    for (uint32_t b = 0; b < nblk; ++b) {
-        if (b * 32 + 32 <= nch && seg_apply(q, blocks[b])) continue;
-        const uint32_t cend = b * 32 + 32 < nch ? b * 32 + 32 : nch;
-        for (uint32_t c = b * 32; c < cend; ++c) {
-            if (seg_apply(q, segs[c])) continue;
-            const uint64_t lo = (uint64_t)c * kSumChunk, hi = umin64(lo + kSumChunk, nvals);
-            for (uint64_t i = lo; i < hi; ++i) q = q + sq_term(v[i]);
+    const HbmSplit sp = hbm_split(a.N);
+    if (t == 0) s_q = 0.0;
+    __syncthreads();
+    uint32_t b0 = 0;  // next block to apply
+    while (true) {
+        if (t == 0) {
+            double q = s_q;
+            uint32_t b = b0;
+            while (b < nblk) {
+                if ((b & 31) == 0 && seg_apply(q, ssup[b >> 5])) {
+                    b += 32;
+                    continue;
+                }
+                if (!seg_apply(q, sblk[b])) break;
+                ++b;
+            }
+            s_q = q;
+            s_fail = b;
         }
+        __syncthreads();
+        const uint32_t fb = s_fail;
+        if (fb >= nblk) break;
+        // stage the failing block's chunk functions and terms
+        const uint32_t c0 = fb * 32, cend = c0 + 32 < nch ? c0 + 32 : nch;
+        if (t < cend - c0) schk[t] = segs[c0 + t];
+        const uint64_t lo = (uint64_t)c0 * kSumChunk, hi = umin64(lo + kBlockTerms, nvals);
+        for (uint64_t i = lo + t; i < hi; i += kWalkThreads) sterm[i - lo] = pool_term(v, i, a.N, sp);
+        __syncthreads();
+        if (t == 0) {
+            double q = s_q;
+            for (uint32_t c = c0; c < cend; ++c) {
+                if (seg_apply(q, schk[c - c0])) continue;
+                const uint64_t l2 = (uint64_t)c * kSumChunk, h2 = umin64(l2 + kSumChunk, nvals);
+                for (uint64_t i = l2; i < h2; ++i) q = q + sterm[i - lo];
+            }
+            s_q = q;
+        }
+        b0 = fb + 1;
+        __syncthreads();
+    }
+    if (t != 0) return;
+    const double q = s_q;
+    if (mode == 1) {
+        a.meta->tracked[buf] = q;
+        return;
     }
     const double rel = fabs(q / a.meta->tracked[buf] - 1.0);
     if (!(rel <= 1e-3))
         a.meta->error = WRNG_GPU_ECORRUPT;
     else
         a.meta->tracked[buf] = q;
-}
-
-size_t hbm_drift_scratch_bytes(uint64_t nvals) {
-    const uint64_t nch = (nvals + kSumChunk - 1) / kSumChunk;
-    return nch * (2 * sizeof(double) + sizeof(int) + sizeof(SumSeg)) +
-           ((nch + 31) / 32) * sizeof(SumSeg) + 1024;
 }
 
 template <typename T>
@@ -336,7 +527,7 @@ __global__ void k_hbm_drift_tree_partial(KernelArgs a, uint32_t buf, uint64_t nv
     const T* v = static_cast<const T*>(a.buf[buf]);
     double q = 0.0;
     for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < nvals; i += gridDim.x * 256ull) {
-        double d = (double)v[i];
+        double d = (double)v[i];  // any order: a storage permutation is irrelevant
         q += d * d;
     }
     red[threadIdx.x] = q;
@@ -360,32 +551,48 @@ __global__ void k_hbm_drift_tree_final(KernelArgs a, uint32_t buf, const double*
         a.meta->tracked[buf] = q;
 }
 
+size_t hbm_drift_scratch_bytes(uint64_t nvals) {
+    const uint64_t nch = (nvals + kSumChunk - 1) / kSumChunk;
+    const uint64_t ncta = (nch + kSumCta - 1) / kSumCta;
+    const size_t sum = (nch + ncta) * sizeof(double) + 128 +
+                       (nch + (nch + 31) / 32) * sizeof(SumSeg) + 1024;
+    const size_t words = (nvals + 2) * sizeof(uint64_t);  // init: uniform words
+    return sum > words ? sum : words;
+}
+
+static cudaError_t exact_sum(uint32_t dtype, const KernelArgs& a, uint32_t buf, int mode,
+                             void* scratch, uint64_t nvals, cudaStream_t st) {
+    const uint32_t nch = (uint32_t)((nvals + kSumChunk - 1) / kSumChunk);
+    const uint32_t ncta = (nch + kSumCta - 1) / kSumCta;
+    double* pre_local = static_cast<double*>(scratch);
+    double* cta_sum = pre_local + nch;
+    SumSeg* segs = reinterpret_cast<SumSeg*>(
+        (reinterpret_cast<uintptr_t>(cta_sum + ncta) + 63) & ~uintptr_t(63));
+    SumSeg* blocks = segs + nch;
+    const uint32_t nblk = (nch + 31) / 32, nsup = (nblk + 31) / 32;
+    const size_t wsm = (nblk + nsup + 32) * sizeof(SumSeg) + kBlockTerms * sizeof(double);
+    cudaFuncSetAttribute(k_sum_walk<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)wsm);
+    cudaFuncSetAttribute(k_sum_walk<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)wsm);
+    if (dtype == WRNG_GPU_F64) {
+        k_sum_chunks<double><<<ncta, kSumCta, 0, st>>>(a, buf, nvals, pre_local, cta_sum, nch);
+        k_sum_segs<double><<<ncta, kSumCta, 0, st>>>(a, buf, nvals, pre_local, cta_sum, segs,
+                                                     blocks, nch);
+        k_sum_walk<double><<<1, kWalkThreads, wsm, st>>>(a, buf, nvals, segs, blocks, nch, mode);
+    } else {
+        k_sum_chunks<float><<<ncta, kSumCta, 0, st>>>(a, buf, nvals, pre_local, cta_sum, nch);
+        k_sum_segs<float><<<ncta, kSumCta, 0, st>>>(a, buf, nvals, pre_local, cta_sum, segs,
+                                                    blocks, nch);
+        k_sum_walk<float><<<1, kWalkThreads, wsm, st>>>(a, buf, nvals, segs, blocks, nch, mode);
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_hbm_drift(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
                              uint32_t buf, int tree, double* scratch, cudaStream_t st) {
     const uint64_t nvals = (uint64_t)n_arrays * a.N;
-    if (!tree) {
-        const uint32_t nch = (uint32_t)((nvals + kSumChunk - 1) / kSumChunk);
-        char* p = reinterpret_cast<char*>(scratch);
-        double* approx = reinterpret_cast<double*>(p);
-        double* pref = approx + nch;
-        int* e = reinterpret_cast<int*>(pref + nch);
-        SumSeg* segs = reinterpret_cast<SumSeg*>(
-            (reinterpret_cast<uintptr_t>(e + nch) + 63) & ~uintptr_t(63));
-        SumSeg* blocks = segs + nch;
-        const uint32_t g = (nch + 255) / 256;
-        if (dtype == WRNG_GPU_F64) {
-            k_sum_chunks<double><<<g, 256, 0, st>>>(a, buf, nvals, approx, nch);
-            k_sum_scan<<<1, 1024, 0, st>>>(approx, nch, e, pref);
-            k_sum_segs<double><<<g, 256, 0, st>>>(a, buf, nvals, e, segs, blocks, nch);
-            k_sum_walk<double><<<1, 32, 0, st>>>(a, buf, nvals, segs, blocks, nch);
-        } else {
-            k_sum_chunks<float><<<g, 256, 0, st>>>(a, buf, nvals, approx, nch);
-            k_sum_scan<<<1, 1024, 0, st>>>(approx, nch, e, pref);
-            k_sum_segs<float><<<g, 256, 0, st>>>(a, buf, nvals, e, segs, blocks, nch);
-            k_sum_walk<float><<<1, 32, 0, st>>>(a, buf, nvals, segs, blocks, nch);
-        }
-        return cudaGetLastError();
-    }
+    if (!tree) return exact_sum(dtype, a, buf, 0, scratch, nvals, st);
     const uint32_t nb = 296;
     if (dtype == WRNG_GPU_F64)
         k_hbm_drift_tree_partial<double><<<nb, 256, 0, st>>>(a, buf, nvals, scratch);
@@ -395,19 +602,21 @@ cudaError_t launch_hbm_drift(uint32_t n_arrays, uint32_t dtype, const KernelArgs
     return cudaGetLastError();
 }
 
-// init_pool / restart of an HBM pool: one CTA generates the n*N + 2 uniforms
-// 256 at a time and writes Box-Muller values straight to the pool buffer.
-template <typename T>
-__global__ void __launch_bounds__(256) k_hbm_init(KernelArgs a, uint32_t buf, int seed_lfg,
-                                                  uint32_t n_arrays) {
+// ---------------------------------------------------------------------------
+// init_pool / restart of an HBM pool (wallace.cpp:158-167, 236):
+//   1 one CTA seeds (or loads) the uniform generator and writes the n*N + 2
+//     uniform words of the pool to scratch, 256 per step;
+//   2 a grid applies Box-Muller to the word pairs (pool values, withheld);
+//   3 tracked = exact direct_sumsq (the sum kernels, mode 1).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_init_words(KernelArgs a, uint64_t nwords, int seed_lfg,
+                                                    uint64_t* words) {
     __shared__ uint64_t tab[608];
     __shared__ uint64_t wbuf[256];
     __shared__ Ctl ctl;
     LfgState* lg = a.lfg;
-    PoolMeta* meta = a.meta;
-    if (!seed_lfg && meta->error) return;
+    if (!seed_lfg && a.meta->error) return;
     if (seed_lfg) {
-        if (threadIdx.x == 0) ctl.active = 0;
         lfg_seed(tab, &ctl, wbuf, a.seed, a.stream0, 256);
     } else {
         for (uint32_t i = threadIdx.x; i < kTable; i += 256) tab[i] = lg->table[i];
@@ -417,33 +626,65 @@ __global__ void __launch_bounds__(256) k_hbm_init(KernelArgs a, uint32_t buf, in
         }
         __syncthreads();
     }
-    T* pool = static_cast<T*>(a.buf[buf]);
-    init_pool_dev(pool, (uint64_t)n_arrays * a.N, tab, &ctl, wbuf, 256);
+    lfg_bulk(tab, &ctl, wbuf, nwords, 256, [&](uint64_t base, uint32_t cnt) {
+        if (threadIdx.x < cnt) words[base + threadIdx.x] = wbuf[threadIdx.x];
+    });
     for (uint32_t i = threadIdx.x; i < kTable; i += 256) lg->table[i] = tab[i];
     if (threadIdx.x == 0) {
         lg->r = ctl.r;
-        lg->draws = ctl.draws;
-        meta->tracked[buf] = ctl.tracked;
-        meta->withheld[buf] = ctl.withheld;
-        meta->avail = 0;
-        if (seed_lfg) {
-            meta->tracked[buf ^ 1u] = 0.0;
-            meta->withheld[buf ^ 1u] = 0.0;
-            meta->active = buf;
-            meta->pass_count = 0;
-            meta->emitted = 0;
-            meta->error = 0;
+        lg->draws = ctl.draws + nwords;
+    }
+}
+
+template <typename T>
+__global__ void k_init_bm(KernelArgs a, uint32_t buf, uint64_t nvals, const uint64_t* words,
+                          int seed_lfg) {
+    if (!seed_lfg && a.meta->error) return;
+    T* pool = static_cast<T*>(a.buf[buf]);
+    const HbmSplit sp = hbm_split(a.N);
+    const uint64_t npairs = nvals / 2 + 1;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < npairs;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        double x, y;
+        box_muller(words[2 * k], words[2 * k + 1], x, y);
+        const uint64_t i = 2 * k;
+        if (i < nvals) {
+            // fill_from_pairs: out = mu + sigma * z with mu = 0, sigma = 1
+            pool[hbm_pos(i, a.N, sp)] = (T)(x + 0.0);
+            pool[hbm_pos(i + 1, a.N, sp)] = (T)(y + 0.0);
+        } else {
+            a.meta->withheld[buf] = x;
         }
     }
 }
 
+__global__ void k_init_meta(PoolMeta* meta, uint32_t buf, int seed_lfg) {
+    if (!seed_lfg && meta->error) return;
+    meta->avail = 0;
+    if (seed_lfg) {
+        meta->tracked[buf ^ 1u] = 0.0;
+        meta->withheld[buf ^ 1u] = 0.0;
+        meta->active = buf;
+        meta->pass_count = 0;
+        meta->emitted = 0;
+        meta->error = 0;
+    }
+}
+
 cudaError_t launch_hbm_init(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
-                            uint32_t buf, int seed_lfg, cudaStream_t st) {
+                            uint32_t buf, int seed_lfg, void* scratch, cudaStream_t st) {
+    const uint64_t nvals = (uint64_t)n_arrays * a.N;
+    uint64_t* words = static_cast<uint64_t*>(scratch);
+    k_init_meta<<<1, 1, 0, st>>>(a.meta, buf, seed_lfg);
+    k_init_words<<<1, 256, 0, st>>>(a, nvals + 2, seed_lfg, words);
+    const uint32_t grid = 148 * 4;
     if (dtype == WRNG_GPU_F64)
-        k_hbm_init<double><<<1, 256, 0, st>>>(a, buf, seed_lfg, n_arrays);
+        k_init_bm<double><<<grid, 256, 0, st>>>(a, buf, nvals, words, seed_lfg);
     else
-        k_hbm_init<float><<<1, 256, 0, st>>>(a, buf, seed_lfg, n_arrays);
-    return cudaGetLastError();
+        k_init_bm<float><<<grid, 256, 0, st>>>(a, buf, nvals, words, seed_lfg);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return exact_sum(dtype, a, buf, 1, scratch, nvals, st);
 }
 
 __global__ void k_setmeta(PoolMeta* meta, uint64_t pass_count, uint64_t avail,

@@ -72,6 +72,10 @@ struct KernelArgs {
     uint64_t drift;        // drift_check_period
     uint64_t seed, stream0;  // OP_INIT
     wrng_gpu_params* params_out;  // OP_PASSES: [pools], params of the last pass
+    // HBM engine: persisting-L2 access window over both pool buffers
+    void* l2_base;
+    uint64_t l2_bytes;
+    float l2_hit;
 };
 
 struct EngineShape {
@@ -103,6 +107,8 @@ cudaError_t launch_hbm_params(uint32_t n_arrays, uint32_t N, LfgState* lfg,
 cudaError_t launch_hbm_pass(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
                             wrng_gpu_params* params, const HbmPass& ps,
                             cudaStream_t st);
+cudaError_t launch_hbm_emit_t(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
+                              uint32_t buf, uint64_t emit_n, uint64_t out_off, cudaStream_t st);
 cudaError_t launch_hbm_emit(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
                             uint32_t buf, uint64_t pos, uint64_t take, uint64_t out_off,
                             cudaStream_t st);
@@ -111,7 +117,27 @@ cudaError_t launch_hbm_drift(uint32_t n_arrays, uint32_t dtype, const KernelArgs
                              uint32_t buf, int tree, double* scratch,
                              cudaStream_t st);
 cudaError_t launch_hbm_init(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
-                            uint32_t buf, int seed_lfg, cudaStream_t st);
+                            uint32_t buf, int seed_lfg, void* scratch, cudaStream_t st);
+
+// Transposed storage of HBM pools: array values i = 0..N-1 stored at
+// (i mod C) * R + i / C with R = 2^lr = min(512, N), C = 2^lc = N / R.
+struct HbmSplit {
+    uint32_t lr, lc;
+};
+__host__ __device__ inline HbmSplit hbm_split(uint32_t N) {
+    uint32_t L = 0;
+    while ((1u << L) < N) ++L;
+    HbmSplit s;
+    s.lr = L < 9 ? L : 9;
+    s.lc = L - s.lr;
+    return s;
+}
+// storage position of flat pool index m*N + i
+__host__ __device__ inline uint64_t hbm_pos(uint64_t flat, uint32_t N, HbmSplit s) {
+    const uint32_t L = s.lr + s.lc;
+    const uint64_t m = flat >> L, i = flat & (N - 1);
+    return (m << L) + ((i & ((1ull << s.lc) - 1)) << s.lr) + (i >> s.lc);
+}
 cudaError_t launch_hbm_setmeta(PoolMeta* meta, uint64_t pass_count, uint64_t avail,
                                uint64_t emitted, uint32_t active, cudaStream_t st);
 
