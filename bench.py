@@ -349,7 +349,8 @@ def main():
     # ---- e2e: same public call, HOST output (pinned), bounded sample -------
     e2e = None
     if rank == 0 or True:
-        n_e2e = min(args.e2e_sample, per_gpu)
+        # per-rank pinned host buffer: 4 GiB at N = 1, 1 GiB per rank at N > 1
+        n_e2e = min(args.e2e_sample if world == 1 else min(args.e2e_sample, 1 << 28), per_gpu)
         host = torch.empty(n_e2e, dtype=out_dtype, pin_memory=True)
         hv = host.numpy()
         gen.fill(hv)  # warm (allocates staging)
