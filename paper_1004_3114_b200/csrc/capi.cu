@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -36,6 +37,10 @@ struct DeviceGuard {
         if (prev >= 0 && cur != prev) cudaSetDevice(prev);
     }
 };
+
+// WRNG_GPU_NO_BULK=1 routes full-refill emission through warp stores (A/B
+// measurements); the default is the bulk-copy engine.
+const bool g_bulk_emit = std::getenv("WRNG_GPU_NO_BULK") == nullptr;
 
 bool crossed(uint64_t before, uint64_t after, uint64_t period) {
     return period > 0 && after / period > before / period;  // wallace.cpp:182-184
@@ -335,6 +340,7 @@ wrng_gpu_status fill_device(wrng_gpu* g, void* out, int out_f32, const OutLayout
         a.mu = mu;
         a.sigma = sigma;
         a.lay = lay;
+        a.bulk_emit = g_bulk_emit && (reinterpret_cast<uintptr_t>(out) % (out_f32 ? 4 : 8)) == 0;
         LAUNCH(launch_smem(g->cfg.n_arrays, g->cfg.dtype, a, s));
         for (uint32_t p = 0; p < P; ++p)
             plan_fill(g, g->ctr[p], lay.len_base + (p < lay.len_extra ? 1 : 0), nullptr);

@@ -21,6 +21,7 @@ namespace wg {
 __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) {
     return a < b ? a : b;
 }
+__device__ __forceinline__ uint32_t umin32(uint32_t a, uint32_t b) { return a < b ? a : b; }
 
 __device__ __forceinline__ double u53(uint64_t w) {
     // next_uniform (uniform.cpp:42-45): top 53 bits * 2^-53
@@ -191,6 +192,8 @@ struct Ctl {
     uint32_t active;
     int32_t error;
     uint32_t have_prev;
+    uint32_t rot;  // smem engine: pool arrays stored rotated by rot (bulk emission)
+    uint32_t pad_;
 };
 
 // Generates `total` words in steps of `step` (<= 256, <= blockDim) into
@@ -443,8 +446,19 @@ __device__ __forceinline__ double sq_term(T v) {
 // chunk (2 KiB).  Must be called by all threads; returns the sum to all.
 constexpr uint32_t kSumScratchBytes = 64 * sizeof(SumSeg);
 
+// A pool whose arrays (length mask + 1) are each stored rotated by `rot`:
+// value i lives at (i & ~mask) | ((i + rot) & mask).
 template <typename T>
-__device__ double exact_sumsq_cta(const T* v, uint32_t n, void* scratch) {
+struct RotView {
+    const T* p;
+    uint32_t mask, rot;
+    __device__ __forceinline__ T operator[](uint32_t i) const {
+        return p[(i & ~mask) | ((i + rot) & mask)];
+    }
+};
+
+template <typename T, typename V = const T*>
+__device__ double exact_sumsq_cta(V v, uint32_t n, void* scratch) {
     const uint32_t nch = blockDim.x < 64 ? blockDim.x : 64;
     uint32_t c = n / nch;  // odd chunk length: conflict-free shared reads
     if (c > 1 && (c & 1) == 0) c -= 1;
@@ -518,7 +532,7 @@ __device__ void init_pool_dev(T* pool, uint64_t nvals, uint64_t* tab, Ctl* ctl,
         }
     });
     // tracked = direct_sumsq (exact left-to-right value, computed in parallel)
-    const double q = exact_sumsq_cta(pool, (uint32_t)nvals, wbuf);
+    const double q = exact_sumsq_cta<T>(pool, (uint32_t)nvals, wbuf);
     if (threadIdx.x == 0) {
         ctl->draws += nvals + 2;
         ctl->tracked = q;

@@ -76,6 +76,9 @@ struct KernelArgs {
     void* l2_base;
     uint64_t l2_bytes;
     float l2_hit;
+    // smem engine: full refills leave shared memory through the bulk-copy
+    // engine (output must be aligned to its element size)
+    uint32_t bulk_emit;
 };
 
 struct EngineShape {

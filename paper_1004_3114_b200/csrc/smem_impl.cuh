@@ -9,14 +9,15 @@
 //      k*NTH (lane-consecutive: odd strides hit 32 distinct banks) and form
 //      the unscaled transform — for n = 4 the scale multiply is the last
 //      rounding of every element (docs/n4_spec.md §3), so the Hadamard /
-//      (J/2 - I) sums need no scale.  Thread 0 meanwhile derives this pass's
-//      chi-squared scale from the previous withheld value
-//      (wallace.cpp:62-65).
-//   C  multiply by the scale, store back in place and, on the last pass of a
-//      refill, stream the exposed values to HBM straight from registers
-//      (coalesced 128-byte warp stores at immediate offsets,
-//      wallace.cpp:206-213).  Warp 0 meanwhile draws the next pass's uniform
-//      words (wallace.cpp:54-58), one word per lane.
+//      (J/2 - I) sums need no scale.  Every thread derives this pass's
+//      chi-squared scale from the broadcast (tracked, withheld)
+//      (wallace.cpp:62-65); warp 0 (all warps compute, warp 0 stores) draws
+//      the next pass's uniform words (wallace.cpp:54-58).
+//   C  multiply by the scale and store back in place.  On the last pass of
+//      a full refill the pool in shared memory is the emitted sequence, and
+//      thread 0 hands it to the bulk-copy engine (cp.async.bulk) after the
+//      pass's final barrier (wallace.cpp:206-213); partial windows and
+//      non-unit outputs use warp stores.  See "bulk-copy emission" below.
 //
 // Addressing: pool accesses are 32-bit shared-window addresses.  When one
 // pool array (N * sizeof(T) bytes) is at most 8 KiB the pool is placed on an
@@ -29,6 +30,9 @@
 
 #include "common.cuh"
 
+#ifndef WG_EXP_NOSTG
+#define WG_EXP_NOSTG 0
+#endif
 #ifndef WG_DATA_REGS
 #define WG_DATA_REGS 64  // registers holding one thread's columns of a pass
 #endif
@@ -123,6 +127,47 @@ __device__ __forceinline__ void emit_one(void* out, uint64_t i, T v, uint32_t ou
 struct EmitCfg {  // per-launch constants of the output stream
     double mu, sigma;
     uint32_t out_f32, unit;
+};
+
+// ---- bulk-copy emission of full refills (unit output) ---------------------
+// Phase C writes the new pool into shared memory anyway, and on a full refill
+// the pool IS the emitted sequence (array-major, wallace.cpp:206-213).  Thread
+// 0 hands it to the bulk-copy engine after the pass's final barrier, so the
+// warps issue no per-value global stores.  cp.async.bulk needs 16-byte
+// alignment on both sides, while a refill's output offset moves by 4N-1
+// values per refill; so the pool is kept ROTATED in shared memory: value j
+// of every array sits at position (j + rot) mod N, with rot chosen on each
+// emitting pass to match the output address modulo 16 bytes.  Gathers fold
+// rot into their offsets (free), phase C stores shift by rot (only the last
+// column group can wrap), and the <= 2*VEC ragged values at each array's
+// ends leave through ordinary stores.  Before the next phase C overwrites
+// the pool, thread 0 waits for the engine's shared-memory reads.
+__device__ __forceinline__ void bulk_store(uint64_t dst, uint32_t src_s, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(src_s), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Where phase C stores and what it emits itself.  my_s: shared address of
+// this thread's column 0 at the new rotation; last_s: of its last column
+// (k = J - 1, the only one that can wrap).  MD 3: values j < j0 and
+// j >= jend[m] (j < N, the withheld slot excluded) are stored by the warps,
+// [j0, jend[m]) by the bulk engine.
+struct PhaseC {
+    uint32_t my_s, last_s;
+    uint32_t j0, jend, jend_last;
 };
 
 // Phase B: gather + unscaled transform (VAR = n=4 matrix variant; AL =
@@ -231,14 +276,44 @@ __device__ __forceinline__ void phase_b2(uint32_t pool_s, uint32_t (&ixb)[4],
     });
 }
 
+// Store of value (m, column group k) into the rotated pool.
+template <typename T, int NA, int LOGN, int M, int K>
+__device__ __forceinline__ void sts_rot(const PhaseC& pc, T v) {
+    using S = SmemShape<T, NA, LOGN>;
+    if constexpr (K == (int)S::J - 1)
+        sts<T, (uint32_t)M * S::ABYTES>(pc.last_s, v);
+    else
+        sts<T, (uint32_t)M * S::ABYTES + (uint32_t)K * S::NTH * (uint32_t)sizeof(T)>(pc.my_s, v);
+}
+
+// MD 3: does this thread store value (m, k) itself (ragged ends)?
+template <typename T, int NA, int LOGN, int M, int K>
+__device__ __forceinline__ bool md3_own(const PhaseC& pc, uint32_t tid) {
+    using S = SmemShape<T, NA, LOGN>;
+    bool own = false;
+    if constexpr (K == 0) own = tid < pc.j0;
+    if constexpr (K == (int)S::J - 1) {
+        const uint32_t j = (uint32_t)K * S::NTH + tid;
+        if constexpr (M == NA - 1)
+            own = own || (j >= pc.jend_last && j != S::N - 1);
+        else
+            own = own || j >= pc.jend;
+    }
+    return own;
+}
+
+// Phase C (packed fp32, n = 4): scale, store in place, emit.  MD 0: no
+// emission; 1: full refill, unit output, warp stores at immediate offsets;
+// 2: partial window / generic output; 3: full refill through the bulk-copy
+// engine (the pool holds the emitted form 0 + v, which differs from v only
+// for v = -0.0; the warps store only the ragged ends).
 template <int LOGN, int EM, int MD>
 __device__ __forceinline__ void phase_c2(const f2_t (&u)[4][SmemShape<float, 4, LOGN>::J / 2],
-                                         float c0, uint32_t pool_s, char* out_p, uint32_t en,
+                                         float c0, const PhaseC& pc, char* out_p, uint32_t en,
                                          const EmitCfg& ec, double& withheld_out) {
     using S = SmemShape<float, 4, LOGN>;
     const uint32_t tid = threadIdx.x;
-    const uint32_t my_s = pool_s + tid * 4u;
-    float* ob = MD == 1 ? reinterpret_cast<float*>(out_p) + tid : nullptr;
+    float* ob = (MD == 1 || MD == 3) ? reinterpret_cast<float*>(out_p) + tid : nullptr;
     const f2_t C = f2_pack(c0, c0), Z = f2_pack(0.0f, 0.0f);
     sfor<0, (int)S::J / 2>([&](auto kc) {
         constexpr int kp = decltype(kc)::value;
@@ -248,14 +323,20 @@ __device__ __forceinline__ void phase_c2(const f2_t (&u)[4][SmemShape<float, 4, 
             float y[2];
             f2_unpack(Y, y[0], y[1]);
             float e[2];
-            if constexpr (MD == 1) f2_unpack(f2_add(Y, Z), e[0], e[1]);  // 0 + 1 * v
+            if constexpr (MD == 1 || MD == 3) f2_unpack(f2_add(Y, Z), e[0], e[1]);  // 0 + 1 * v
             sfor<0, 2>([&](auto hc) {
                 constexpr int h = decltype(hc)::value;
                 constexpr int k = 2 * kp + h;
                 constexpr uint32_t col = m * S::N + k * S::NTH;
-                sts<float, col * 4u>(my_s, y[h]);
-                if constexpr (MD == 1) {
+                sts_rot<float, 4, LOGN, m, k>(pc, MD == 3 ? e[h] : y[h]);
+                if constexpr (MD == 3) {
+                    if constexpr (k == 0 || k == (int)S::J - 1) {
+                        if (md3_own<float, 4, LOGN, m, k>(pc, tid)) ob[col] = e[h];
+                    }
+                } else if constexpr (MD == 1) {
+#if !WG_EXP_NOSTG  // experiment only: drop the output stores to bound their cost
                     if (!(m == 3 && k == (int)S::J - 1) || tid != S::NTH - 1) ob[col] = e[h];
+#endif
                 } else if constexpr (MD == 2) {
                     const uint32_t flat = col + tid;
                     if (flat < en)
@@ -267,19 +348,17 @@ __device__ __forceinline__ void phase_c2(const f2_t (&u)[4][SmemShape<float, 4, 
             });
         });
     });
+    if constexpr (MD == 3) fence_async_smem();  // generic -> async proxy
 }
 
-// Phase C: scale, store in place, emit.  MD 0: no emission; 1: the whole
-// exposed pool (all but the withheld slot) with unit output: unconditional
-// stores at immediate offsets; 2: partial window / generic output.
+// Phase C, generic (fp64 pools, n = 2, odd J): as phase_c2.
 template <typename T, int NA, int LOGN, int EM, int MD>
 __device__ __forceinline__ void phase_c(const T (&u)[NA][SmemShape<T, NA, LOGN>::J], T c0, T c1,
-                                        uint32_t pool_s, char* out_p, uint32_t en,
+                                        const PhaseC& pc, char* out_p, uint32_t en,
                                         const EmitCfg& ec, double& withheld_out) {
     using S = SmemShape<T, NA, LOGN>;
     const uint32_t tid = threadIdx.x;
-    const uint32_t my_s = pool_s + tid * (uint32_t)sizeof(T);
-    T* ob = MD == 1 ? reinterpret_cast<T*>(out_p) + tid : nullptr;
+    T* ob = (MD == 1 || MD == 3) ? reinterpret_cast<T*>(out_p) + tid : nullptr;
     sfor<0, (int)S::J>([&](auto kc) {
         constexpr int k = decltype(kc)::value;
         T y[NA];
@@ -295,7 +374,15 @@ __device__ __forceinline__ void phase_c(const T (&u)[NA][SmemShape<T, NA, LOGN>:
         sfor<0, NA>([&](auto mc) {
             constexpr int m = decltype(mc)::value;
             constexpr uint32_t col = m * S::N + k * S::NTH;
-            sts<T, col * (uint32_t)sizeof(T)>(my_s, y[m]);
+            if constexpr (MD == 3) {
+                const T e = y[m] + (T)0;  // 0 + 1 * v: the pool is the bulk source
+                sts_rot<T, NA, LOGN, m, k>(pc, e);
+                if constexpr (k == 0 || k == (int)S::J - 1) {
+                    if (md3_own<T, NA, LOGN, m, k>(pc, tid)) ob[col] = e;
+                }
+            } else {
+                sts_rot<T, NA, LOGN, m, k>(pc, y[m]);
+            }
             if constexpr (MD == 1) {
                 if (!(m == NA - 1 && k == (int)S::J - 1) || tid != S::NTH - 1)
                     ob[col] = y[m] + (T)0;  // 0 + 1 * v
@@ -307,6 +394,48 @@ __device__ __forceinline__ void phase_c(const T (&u)[NA][SmemShape<T, NA, LOGN>:
         });
         if (k == (int)S::J - 1 && tid == S::NTH - 1) withheld_out = (double)y[NA - 1];
     });
+    if constexpr (MD == 3) fence_async_smem();
+}
+
+template <int LOGN, int EM>
+__device__ __forceinline__ void phase_c2_any(uint32_t md,
+                                             const f2_t (&u)[4][SmemShape<float, 4, LOGN>::J / 2],
+                                             float c0, const PhaseC& pc, char* out_p, uint32_t en,
+                                             const EmitCfg& ec, double& wh) {
+    if (md == 0)
+        phase_c2<LOGN, EM, 0>(u, c0, pc, out_p, 0, ec, wh);
+    else if (EM == EM_UNIT && md == 3)
+        phase_c2<LOGN, EM, 3>(u, c0, pc, out_p, en, ec, wh);
+    else if (EM == EM_UNIT && md == 1)
+        phase_c2<LOGN, EM, 1>(u, c0, pc, out_p, en, ec, wh);
+    else
+        phase_c2<LOGN, EM, 2>(u, c0, pc, out_p, en, ec, wh);
+}
+
+template <typename T, int NA, int LOGN, int EM>
+__device__ __forceinline__ void phase_c_any(uint32_t md,
+                                            const T (&u)[NA][SmemShape<T, NA, LOGN>::J], T c0,
+                                            T c1, const PhaseC& pc, char* out_p, uint32_t en,
+                                            const EmitCfg& ec, double& wh) {
+    if (md == 0)
+        phase_c<T, NA, LOGN, EM, 0>(u, c0, c1, pc, out_p, 0, ec, wh);
+    else if (EM == EM_UNIT && md == 3)
+        phase_c<T, NA, LOGN, EM, 3>(u, c0, c1, pc, out_p, en, ec, wh);
+    else if (EM == EM_UNIT && md == 1)
+        phase_c<T, NA, LOGN, EM, 1>(u, c0, c1, pc, out_p, en, ec, wh);
+    else
+        phase_c<T, NA, LOGN, EM, 2>(u, c0, c1, pc, out_p, en, ec, wh);
+}
+
+// The phase B -> C barrier; with bulk emission on, thread 0 first waits
+// until the previous refill's bulk copies have read the pool (phase C
+// rewrites it).
+template <int EM>
+__device__ __forceinline__ void bc_barrier(bool bulk_on) {
+    if constexpr (EM == EM_UNIT) {
+        if (bulk_on && threadIdx.x == 0) bulk_wait_read();
+    }
+    __syncthreads();
 }
 
 // One in-place regeneration pass.  Preconditions (after a barrier): the
@@ -322,19 +451,21 @@ __device__ __forceinline__ void phase_c(const T (&u)[NA][SmemShape<T, NA, LOGN>:
 template <typename T, int NA, int LOGN, int EM, bool AL, bool COLD>
 __device__ __forceinline__ bool smem_pass(uint32_t pool_s, uint32_t mode, uint32_t emit_n,
                                           char* out_p, const EmitCfg& ec, wrng_gpu_params* rec,
-                                          bool prefetch, T* prev, int slot) {
+                                          bool prefetch, T* prev, int slot, bool bulk_on) {
     using S = SmemShape<T, NA, LOGN>;
     constexpr uint32_t N = S::N, NTH = S::NTH;
     const uint32_t tid = threadIdx.x;
     Ctl* ctl = &sm_at<Ctl>(S::CTL_OFF);
     const LfgParams& cp = slot ? ctl->cur2 : ctl->cur;
+    constexpr uint32_t ES = (uint32_t)sizeof(T);
+    const uint32_t rot = ctl->rot;  // value j of each array sits at (j + rot) mod N
 
     uint32_t ixb[NA], stepb[NA];
 #pragma unroll
     for (int m = 0; m < NA; ++m) {
         const uint32_t st = cp.stride[m];
-        ixb[m] = (st * tid + cp.offset[m]) * (uint32_t)sizeof(T);
-        stepb[m] = st * NTH * (uint32_t)sizeof(T);
+        ixb[m] = (st * tid + cp.offset[m] + rot) * ES;
+        stepb[m] = st * NTH * ES;
     }
     const uint32_t variant = cp.variant;
     const double tracked = ctl->tracked, withheld = ctl->withheld;
@@ -370,47 +501,66 @@ __device__ __forceinline__ bool smem_pass(uint32_t pool_s, uint32_t mode, uint32
     }
     if (COLD && prev) {
         // the pre-pass pool becomes the inactive buffer (wallace.cpp:170-174)
-        constexpr uint32_t NVEC = (uint32_t)(S::NVALS * sizeof(T) / 16);
-        uint4* dst = reinterpret_cast<uint4*>(prev);
-        for (uint32_t i = tid; i < NVEC; i += NTH) dst[i] = sm_at<uint4>(S::POOL_OFF + i * 16);
+        const RotView<T> v{&sm_at<T>(S::POOL_OFF), S::MASK, rot};
+        for (uint32_t i = tid; i < (uint32_t)S::NVALS; i += NTH) prev[i] = v[i];
     }
     if (prefetch)
         draw_pass_params_all<NA>(&sm_at<uint64_t>(S::TAB_OFF), ctl, N, slot ^ 1, tid < 32);
     const T c0 = (T)c0d, c1 = (T)c1d;  // fp32 pools: rounded once (docs/n4_spec.md §4)
     double wh = 0.0;
+    const uint32_t md = emit_n == 0                                    ? 0u
+                        : (EM == EM_UNIT && emit_n == (uint32_t)S::CAP) ? (bulk_on ? 3u : 1u)
+                                                                        : 2u;
+    // new rotation: on a bulk-emitting pass, the output's 16-byte phase
+    constexpr uint32_t VEC = 16 / ES;
+    const uint32_t rot2 =
+        md == 3 ? (uint32_t)(reinterpret_cast<uintptr_t>(out_p) / ES) & (VEC - 1) : rot;
+    PhaseC pc;
+    pc.my_s = pool_s + (tid + rot2) * ES;
+    {
+        const uint32_t lastb = (((uint32_t)(S::J - 1) * NTH + tid + rot2) * ES) & S::MASKB;
+        pc.last_s = AL ? (lastb | pool_s) : (lastb + pool_s);
+    }
+    pc.j0 = (VEC - rot2) & (VEC - 1);
+    pc.jend = pc.j0 + ((N - rot2 - pc.j0) & ~(VEC - 1));
+    pc.jend_last = pc.j0 + ((umin32(N - rot2, N - 1) - pc.j0) & ~(VEC - 1));
     if constexpr (sizeof(T) == 4 && NA == 4 && S::J % 2 == 0) {
         f2_t u[4][S::J / 2];
         if (variant == 0)
             phase_b2<LOGN, 0, AL>(pool_s, ixb, stepb, u);
         else
             phase_b2<LOGN, 1, AL>(pool_s, ixb, stepb, u);
-        __syncthreads();
-        if (emit_n == 0)
-            phase_c2<LOGN, EM, 0>(u, c0, pool_s, out_p, 0, ec, wh);
-        else if (EM == EM_UNIT && emit_n == (uint32_t)S::CAP)
-            phase_c2<LOGN, EM, 1>(u, c0, pool_s, out_p, emit_n, ec, wh);
-        else
-            phase_c2<LOGN, EM, 2>(u, c0, pool_s, out_p, emit_n, ec, wh);
+        bc_barrier<EM>(bulk_on);
+        phase_c2_any<LOGN, EM>(md, u, c0, pc, out_p, emit_n, ec, wh);
     } else {
         T u[NA][S::J];
         if (NA == 2 || variant == 0)
             phase_b<T, NA, LOGN, 0, AL>(pool_s, ixb, stepb, u);
         else
             phase_b<T, NA, LOGN, 1, AL>(pool_s, ixb, stepb, u);
-        __syncthreads();
-        if (emit_n == 0)
-            phase_c<T, NA, LOGN, EM, 0>(u, c0, c1, pool_s, out_p, 0, ec, wh);
-        else if (EM == EM_UNIT && emit_n == (uint32_t)S::CAP)
-            phase_c<T, NA, LOGN, EM, 1>(u, c0, c1, pool_s, out_p, emit_n, ec, wh);
-        else
-            phase_c<T, NA, LOGN, EM, 2>(u, c0, c1, pool_s, out_p, emit_n, ec, wh);
+        bc_barrier<EM>(bulk_on);
+        phase_c_any<T, NA, LOGN, EM>(md, u, c0, c1, pc, out_p, emit_n, ec, wh);
     }
     if (tid == NTH - 1) ctl->withheld = wh;  // wallace.cpp:136
     if (tid == 0) {
         ctl->tracked = target;  // wallace.cpp:135
         ctl->active ^= 1u;
+        ctl->rot = rot2;
     }
     __syncthreads();
+    if (md == 3 && tid == 0) {
+        // [j0, jend) of every array (last: jend_last) -> output, 16-byte aligned
+        const uint64_t ob = reinterpret_cast<uint64_t>(out_p);
+#pragma unroll
+        for (int m = 0; m < NA; ++m) {
+            const uint32_t je = m == NA - 1 ? pc.jend_last : pc.jend;
+            if (je > pc.j0)
+                bulk_store(ob + ((uint64_t)m * N + pc.j0) * ES,
+                           pool_s + (uint32_t)m * S::ABYTES + (pc.j0 + rot2) * ES,
+                           (je - pc.j0) * ES);
+        }
+        bulk_commit();
+    }
     return true;
 }
 
@@ -419,8 +569,8 @@ __device__ __forceinline__ bool smem_drift_check() {
     // wallace.cpp:225-234 with Pool::direct_sumsq order (wallace.cpp:13-18)
     using S = SmemShape<T, NA, LOGN>;
     Ctl* ctl = &sm_at<Ctl>(S::CTL_OFF);
-    const double rec = exact_sumsq_cta(&sm_at<T>(S::POOL_OFF), (uint32_t)S::NVALS,
-                                       &sm_at<uint64_t>(S::WBUF_OFF));
+    const RotView<T> v{&sm_at<T>(S::POOL_OFF), S::MASK, ctl->rot};
+    const double rec = exact_sumsq_cta<T>(v, (uint32_t)S::NVALS, &sm_at<uint64_t>(S::WBUF_OFF));
     if (threadIdx.x == 0) {
         const double rel = fabs(rec / ctl->tracked - 1.0);
         if (!(rel <= 1e-3))
@@ -437,6 +587,8 @@ __device__ __forceinline__ void smem_restart() {
     using S = SmemShape<T, NA, LOGN>;
     init_pool_dev(&sm_at<T>(S::POOL_OFF), S::NVALS, &sm_at<uint64_t>(S::TAB_OFF),
                   &sm_at<Ctl>(S::CTL_OFF), &sm_at<uint64_t>(S::WBUF_OFF), S::STEP);
+    if (threadIdx.x == 0) sm_at<Ctl>(S::CTL_OFF).rot = 0;  // natural order again
+    __syncthreads();
 }
 
 // Passes-until-boundary bookkeeping without divisions in the refill loop:
@@ -488,6 +640,7 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
             ctl->have_prev = 0;
             ctl->cur.c = ctl->cur.s = ctl->cur2.c = ctl->cur2.s = 0.0;
             ctl->cur.pad_ = ctl->cur2.pad_ = 0;
+            ctl->rot = 0;
         }
         lfg_seed(tab, ctl, wbuf, a.seed, a.stream0 + p, S::STEP);
     } else {
@@ -506,6 +659,7 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
             ctl->have_prev = 0;
             ctl->cur.c = ctl->cur.s = ctl->cur2.c = ctl->cur2.s = 0.0;
             ctl->cur.pad_ = ctl->cur2.pad_ = 0;
+            ctl->rot = 0;
         }
         const uint4* src = reinterpret_cast<const uint4*>(static_cast<const T*>(a.buf[act]) +
                                                           (uint64_t)p * NVALS);
@@ -520,6 +674,7 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
     const uint32_t f = a.f;
     const uint32_t mode = a.mode;
     const EmitCfg ec{a.mu, a.sigma, a.out_f32, a.unit};
+    const bool bulk_on = EM == EM_UNIT && op == OP_FILL && a.bulk_emit != 0;
     PeriodCounter drift, restart;
     drift.init(a.drift, pc);
     restart.init(a.restart, pc);
@@ -594,9 +749,9 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
             const bool ok =
                 last_launch
                     ? smem_pass<T, NA, LOGN, EM, AL, true>(pool_s, mode, en, out_p, ec, nullptr,
-                                                           prefetch, prev_buf(), slot)
+                                                           prefetch, prev_buf(), slot, bulk_on)
                     : smem_pass<T, NA, LOGN, EM, AL, false>(pool_s, mode, en, out_p, ec, nullptr,
-                                                            prefetch, nullptr, slot);
+                                                            prefetch, nullptr, slot, bulk_on);
             if (!ok) {
                 err = ctl->error;
                 break;
@@ -634,8 +789,9 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
             const bool last_launch = pass_i == total_passes;
             wrng_gpu_params* rec = (a.params_out && last_launch) ? a.params_out + p : nullptr;
             if (!smem_pass<T, NA, LOGN, EM, AL, true>(pool_s, mode, 0u, nullptr, ec, rec,
-                                                !last_launch,
-                                                last_launch ? prev_buf() : nullptr, slot)) {
+                                                      !last_launch,
+                                                      last_launch ? prev_buf() : nullptr, slot,
+                                                      false)) {
                 err = ctl->error;
                 break;
             }
@@ -653,13 +809,18 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
     }
 
     // ---- write back -------------------------------------------------------
+    if (bulk_on && tid == 0) bulk_wait_all();  // bulk copies complete before exit
     __syncthreads();
     const uint32_t act = ctl->active;
-    {
+    if (ctl->rot == 0) {
         uint4* dst =
             reinterpret_cast<uint4*>(static_cast<T*>(a.buf[act]) + (uint64_t)p * NVALS);
         constexpr uint32_t NVEC = (uint32_t)(NVALS * sizeof(T) / 16);
         for (uint32_t i = tid; i < NVEC; i += NTH) dst[i] = sm_at<uint4>(S::POOL_OFF + i * 16);
+    } else {  // back to natural order
+        T* dst = static_cast<T*>(a.buf[act]) + (uint64_t)p * NVALS;
+        const RotView<T> v{&sm_at<T>(S::POOL_OFF), S::MASK, ctl->rot};
+        for (uint32_t i = tid; i < (uint32_t)NVALS; i += NTH) dst[i] = v[i];
     }
     for (uint32_t i = tid; i < kTable; i += NTH) lg->table[i] = tab[i];
     if (tid == 0) {
