@@ -6,6 +6,13 @@
 //   mode 1: bulk-copy engine (thread 0: cp.async.bulk from a 16 KiB shared
 //           buffer, 16-byte aligned part only; ragged ends skipped)
 //   mode 2: plain fill over the whole range, 1184 x 256 threads, float4
+//   mode 3: as 2 with 256-bit stores (st.global.v8.f32)
+//   mode 4: as 2, float4 with the streaming hint (st.global.cs)
+//   mode 5: as 1 with 8 bulk groups in flight per CTA
+//   mode 6: one-shot grid, 128 threads x 16 float4 per block (32 KiB chunk)
+//   mode 7: as 1 but CTA p starts at chunk (37 p) mod nchunks (decorrelated)
+//   mode 8+: bulk, aligned chunks of CB bytes, P2 CTAs, queue Q, optional
+//            L2 evict_first hint (see table in main)
 // nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a scripts/seg_write_peak.cu -o scripts/seg_write_peak.bin
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -47,6 +54,100 @@ __global__ void __launch_bounds__(64) k_bulk(float* out, uint64_t seg) {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+__global__ void __launch_bounds__(64) k_bulk8(float* out, uint64_t seg) {
+    extern __shared__ __align__(1024) float sm[];
+    for (int i = threadIdx.x; i < 4096; i += 64) sm[i] = (float)blockIdx.x;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    float* o = out + (uint64_t)blockIdx.x * seg;
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(sm);
+    for (uint64_t done = 0; done < seg; done += kChunk) {
+        const uint64_t n = seg - done < kChunk ? seg - done : kChunk;
+        uint64_t a = reinterpret_cast<uint64_t>(o + done);
+        const uint64_t e = reinterpret_cast<uint64_t>(o + done + n) & ~15ull;
+        a = (a + 15) & ~15ull;
+        if (e > a) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(a),
+                         "r"(s), "r"((uint32_t)(e - a))
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 7;" ::: "memory");
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(64) k_bulk_rot(float* out, uint64_t seg) {
+    extern __shared__ __align__(1024) float sm[];
+    for (int i = threadIdx.x; i < 4096; i += 64) sm[i] = (float)blockIdx.x;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    float* o = out + (uint64_t)blockIdx.x * seg;
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(sm);
+    const uint64_t nch = seg / kChunk;
+    for (uint64_t c = 0; c < nch; ++c) {
+        const uint64_t done = ((c + 37ull * blockIdx.x) % nch) * kChunk;
+        uint64_t a = reinterpret_cast<uint64_t>(o + done);
+        const uint64_t e = reinterpret_cast<uint64_t>(o + done + kChunk) & ~15ull;
+        a = (a + 15) & ~15ull;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(a),
+                     "r"(s), "r"((uint32_t)(e - a))
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+template <int HINT>
+__global__ void __launch_bounds__(32) k_bulk_gen(char* out, uint64_t seg, uint32_t cb, int q) {
+    extern __shared__ __align__(1024) float sm[];
+    for (uint32_t i = threadIdx.x; i < cb / 4; i += 32) sm[i] = (float)blockIdx.x;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    char* o = out + (uint64_t)blockIdx.x * seg;
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(sm);
+    uint64_t pol = 0;
+    if (HINT) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    for (uint64_t done = 0; done + cb <= seg; done += cb) {
+        if (HINT)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                         ::"l"(o + done), "r"(s), "r"(cb), "l"(pol) : "memory");
+        else
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(o + done),
+                         "r"(s), "r"(cb) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (q <= 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        else asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+__global__ void k_fill8(float* out, uint64_t n8) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n8;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        asm volatile("st.global.v8.f32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(out + 8 * i),
+                     "f"(1.0f)
+                     : "memory");
+}
+
+__global__ void k_fill_cs(float4* out, uint64_t n4) {
+    const float4 v = make_float4(1.f, 2.f, 3.f, 4.f);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        __stcs(out + i, v);
+}
+
+__global__ void __launch_bounds__(128) k_chunk(float4* out) {
+    const float4 v = make_float4(1.f, 2.f, 3.f, 4.f);
+    float4* o = out + (uint64_t)blockIdx.x * 2048 + threadIdx.x;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) o[128 * i] = v;
+}
+
 __global__ void k_fill(float4* out, uint64_t n4) {
     const float4 v = make_float4(1.f, 2.f, 3.f, 4.f);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4;
@@ -67,13 +168,46 @@ int main(int argc, char** argv) {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    for (int mode = 0; mode < 3; ++mode) {
+    cudaFuncSetAttribute(k_bulk8, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384);
+    cudaFuncSetAttribute(k_bulk_rot, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384);
+    cudaFuncSetAttribute(k_bulk_gen<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    cudaFuncSetAttribute(k_bulk_gen<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    // mode 8..: {chunk bytes, CTAs per SM, queue, hint}
+    const int gen[][4] = {{16384, 8, 4, 0}, {4096, 8, 4, 0}, {65536, 2, 4, 0}, {16384, 8, 4, 1},
+                          {16384, 4, 4, 0}, {16384, 14, 4, 0}, {32768, 6, 4, 0}, {16384, 8, 1, 0}};
+    for (int mode = 0; mode < 16; ++mode) {
+        if (mode >= 8) {
+            const int* gcfg = gen[mode - 8];
+            const int P2 = 148 * gcfg[1];
+            const uint64_t seg2 = (total * 4 / P2) & ~65535ull;
+            float best = 1e30f;
+            for (int rep = 0; rep < 4; ++rep) {
+                cudaEventRecord(a);
+                if (gcfg[3]) k_bulk_gen<1><<<P2, 32, gcfg[0]>>>((char*)out, seg2, gcfg[0], gcfg[2]);
+                else k_bulk_gen<0><<<P2, 32, gcfg[0]>>>((char*)out, seg2, gcfg[0], gcfg[2]);
+                cudaEventRecord(b);
+                cudaEventSynchronize(b);
+                float ms = 0;
+                cudaEventElapsedTime(&ms, a, b);
+                if (rep > 0 && ms < best) best = ms;
+            }
+            cudaError_t e = cudaGetLastError();
+            printf("{\"mode\": %d, \"chunk\": %d, \"ctas_per_sm\": %d, \"queue\": %d, \"hint\": %d, \"ms\": %.3f, \"gbs\": %.1f, \"err\": \"%s\"}\n",
+                   mode, gcfg[0], gcfg[1], gcfg[2], gcfg[3], best,
+                   (double)(P2 * (seg2 / gcfg[0]) * gcfg[0]) / (best / 1e3) / 1e9, cudaGetErrorString(e));
+            continue;
+        }
         float best = 1e30f;
         for (int rep = 0; rep < 5; ++rep) {
             cudaEventRecord(a);
             if (mode == 0) k_warp<<<P, 64>>>(out, seg);
             if (mode == 1) k_bulk<<<P, 64, 16384>>>(out, seg);
             if (mode == 2) k_fill<<<P, 256>>>(reinterpret_cast<float4*>(out), total / 4);
+            if (mode == 3) k_fill8<<<P, 256>>>(out, total / 8);
+            if (mode == 4) k_fill_cs<<<P, 256>>>(reinterpret_cast<float4*>(out), total / 4);
+            if (mode == 5) k_bulk8<<<P, 64, 16384>>>(out, seg);
+            if (mode == 7) k_bulk_rot<<<P, 64, 16384>>>(out, seg);
+            if (mode == 6) k_chunk<<<(unsigned)(total / 8192), 128>>>(reinterpret_cast<float4*>(out));
             cudaEventRecord(b);
             cudaEventSynchronize(b);
             float ms = 0;
