@@ -274,6 +274,81 @@ def test_device_tensor_fill_equals_host_fill(W):
     assert_bits(t.cpu().numpy(), g2.fill(t.numel()))
 
 
+# Bulk-copy emission (smem engine, unit output): the pool is kept rotated in
+# shared memory to match the output's 16-byte phase; every phase, ragged
+# ends, leftovers across calls, drift audits and restarts on a rotated pool.
+@pytest.mark.parametrize("dt,n,p", [("f32", 4, 10), ("f32", 2, 8), ("f64", 2, 10),
+                                    ("f64", 4, 12), ("f32", 4, 13), ("f64", 4, 8)])
+def test_bulk_emission_every_output_phase(W, dt, n, p):
+    import torch
+
+    pools = 3
+    tdt = torch.float32 if dt == "f32" else torch.float64
+    odt = O.F32 if dt == "f32" else O.F64
+    cap = n * (1 << p) - 1
+    counts = (pools * (3 * cap + 7), pools * (cap + 1) + 2)  # full refills, tails, leftovers
+    vec = 4 if dt == "f32" else 2
+    for off in range(vec):
+        # (restarts re-initialise with the device Box-Muller, which is only
+        # tolerance-equal to glibc: covered bulk-vs-warp-store below)
+        kw = dict(pool_exponent=p, throwaway_f=1, seed=5 + off, n_arrays=n, dtype=dt, pools=pools,
+                  init_on_host=True, drift_check_period=2)
+        g = gpu_state(W, **kw)
+        orc = [O.OracleState(pool_exponent=p, throwaway_f=1, seed=5 + off, stream=q, n_arrays=n,
+                             dtype=odt, drift_period=2) for q in range(pools)]
+        for c in counts:
+            buf = torch.full((c + vec,), 7.0, dtype=tdt, device="cuda")
+            g.fill(buf[off:off + c])
+            torch.cuda.synchronize()
+            got = buf.cpu().numpy()
+            assert np.all(got[:off] == 7.0) and np.all(got[off + c:] == 7.0), "wrote outside"
+            got = got[off:off + c]
+            per, extra = divmod(c, pools)
+            base = 0
+            for q in range(pools):
+                ln = per + (1 if q < extra else 0)
+                assert_bits(got[base:base + ln], orc[q].fill(ln))
+                base += ln
+        # the pool written back after rotated emission is in natural order
+        for q in range(pools):
+            gp = g.active_pool(q)
+            ov, ot, ow = orc[q].pool()
+            assert_bits(gp.arrays.reshape(-1), ov)
+            assert (gp.tracked_sumsq, gp.withheld) == (ot, ow)
+
+
+@pytest.mark.parametrize("dt,n", [("f32", 4), ("f64", 2)])
+def test_bulk_and_warp_store_emission_agree(W, dt, n):
+    """WRNG_GPU_NO_BULK switches full-refill emission to warp stores; both
+    paths must produce the same bits, through drift audits and restarts on a
+    rotated pool (subprocess: the switch is read when the library loads)."""
+    import subprocess
+    import sys
+
+    tdt = "torch.float32" if dt == "f32" else "torch.float64"
+    code = (
+        "import numpy as np, torch, hashlib\n"
+        "import paper_1004_3114_b200 as W\n"
+        f"g = W.WallaceState(W.WallaceConfig(pool_exponent=10, throwaway_f=1, seed=3, n_arrays={n},"
+        f" dtype='{dt}', pools=37, drift_check_period=2, restart_interval_passes=3))\n"
+        f"t = torch.empty(37 * 20000 + 11, dtype={tdt}, device='cuda')\n"
+        "h = hashlib.sha256()\n"
+        "for a, b in ((1, 37 * 9000 + 2), (37 * 9000 + 2, 37 * 20000 + 11)):\n"
+        "    g.fill(t[a:b]); torch.cuda.synchronize(); h.update(t[a:b].cpu().numpy().tobytes())\n"
+        "p = g.active_pool(5)\n"
+        "h.update(p.arrays.tobytes()); h.update(np.array([p.tracked_sumsq, p.withheld]).tobytes())\n"
+        "print(h.hexdigest())\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ({}, {"WRNG_GPU_NO_BULK": "1"}):
+        e = dict(os.environ, **env)
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=e, capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        outs.append(r.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1]
+
+
 def test_host_fill_larger_than_staging(W):
     """Host output larger than the 2 x 256 MiB staging slabs (f32 bank)."""
     g = gpu_state(W, pool_exponent=10, throwaway_f=1, seed=31, n_arrays=4, dtype="f32", pools=148,
