@@ -188,6 +188,45 @@ wrng_gpu_status wrng_gpu_moments_f32(const float* dev, uint64_t n, double* out5,
 wrng_gpu_status wrng_gpu_moments_f64(const double* dev, uint64_t n, double* out5,
                                      int32_t device, void* stream);
 
+/* ---- validation statistics on the device ------------
+ * u/v uniformity counts of a DEVICE array of n normals: pairs
+ * (v[2i], v[2i+1]) -> to_uv (stats.cpp:10-16) -> k bins of u on [0, 1] and
+ * of v on [-pi/2, pi/2] (chi2_bins, stats.cpp:18-38), paired as the CLI's
+ * uniformity test does (tools/main.cpp:160-193); (0, 0) pairs are skipped.
+ * counts_u / counts_v: host arrays of k, overwritten.  1 < k <= 8192.
+ * Synchronous. */
+wrng_gpu_status wrng_gpu_uv_counts(const void* dev, int32_t is_f32, uint64_t n, uint32_t k,
+                                   uint64_t* counts_u, uint64_t* counts_v, uint64_t* skipped,
+                                   int32_t device, void* stream);
+/* autocorr_at_lag (stats.cpp:110-127) of a DEVICE array, from one-pass raw
+ * sums (sum z_t z_{t+lag}, sum z_t, sum z_{t+lag}, sum z_t^2) and the mean.
+ * EINVAL unless n >= lag + 2.  Synchronous. */
+wrng_gpu_status wrng_gpu_autocorr(const void* dev, int32_t is_f32, uint64_t n, uint64_t lag,
+                                  double* r, int32_t device, void* stream);
+/* chi2_sf (stats.cpp:40-87): survival function of chi-squared(dof). */
+double wrng_gpu_chi2_sf(double statistic, uint32_t dof);
+
+/* Generate-and-check with no host copy of the values: advances every pool
+ * exactly as wrng_gpu_fill_*(g, count) would (pool p: count / pools values,
+ * one more for p < count % pools), generating into an L2-sized device slab
+ * and reducing each slab on the device.  Pairs (u/v) and lags (autocorr)
+ * are taken within each pool's stream; statistics are pooled over pools
+ * (for one pool they are the reference's, stats.cpp / tools/main.cpp).
+ * counts_u / counts_v: optional host arrays of k. */
+typedef struct wrng_gpu_validation {
+    uint64_t n;                       /* values generated and checked */
+    double m1, m2, m3, m4;            /* moments (stats.cpp:89-108 + m3) */
+    double z1, z2, z4;                /* standardized deviations (stats.cpp:103-105) */
+    uint64_t uv_samples, uv_skipped;  /* pairs binned / (0, 0) pairs skipped */
+    uint32_t k, dof;                  /* bins, k - 1 */
+    double u_statistic, u_p, v_statistic, v_p;  /* chi2_bins of u and v */
+    uint64_t lag;
+    double autocorr;                  /* r at lag */
+} wrng_gpu_validation;
+wrng_gpu_status wrng_gpu_validate(wrng_gpu_t* g, uint64_t count, uint32_t k, uint64_t lag,
+                                  uint64_t* counts_u, uint64_t* counts_v,
+                                  wrng_gpu_validation* out);
+
 /* Device uniform generator, for bit-exact stream checks: the first `count`
  * next_word() outputs of UniformState(seed, stream_id + p) for p < pools,
  * pool-major (uniform.cpp:23-40). */

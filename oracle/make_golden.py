@@ -93,6 +93,19 @@ def ref_golden():
     L = O.ref_lib()
     out["chi2_target_0_2048"] = L.ref_chi2_target(0.0, 2048)
     out["chi2_target_1_2048"] = L.ref_chi2_target(1.0, 2048)
+    # validation statistics of a reference stream (stats.cpp:10-127, the
+    # CLI's u/v pairing tools/main.cpp:160-193)
+    st = O.RefState(pool_exponent=10, throwaway_f=3, seed=1)
+    v = st.fill(200000)
+    uv = O.ref_uv_chi2(v, 1000)
+    out["stats"] = {
+        "stream": {"pool_exponent": 10, "throwaway_f": 3, "seed": 1, "count": 200000,
+                   "sha256": h(v)},
+        "uv_k1000": uv,
+        "autocorr": {str(lag): O.ref_autocorr(v, lag) for lag in (1, 2, 5, 100)},
+        "chi2_sf": [[x, d, O.ref_chi2_sf(x, d)] for x, d in
+                    ((1000.0, 999), (50.0, 10), (0.5, 3), (842.0, 999), (1156.0, 999))],
+    }
     return out
 
 

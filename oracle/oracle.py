@@ -123,6 +123,19 @@ def oracle_lib():
         lib.or_anderson_darling_f64.argtypes = [vp, C.c_size_t]
         lib.or_anderson_darling_f32.restype = dbl
         lib.or_anderson_darling_f32.argtypes = [vp, C.c_size_t]
+        lib.or_to_uv.argtypes = [dbl, dbl, C.POINTER(dbl), C.POINTER(dbl)]
+        lib.or_chi2_bin.restype = C.c_int64
+        lib.or_chi2_bin.argtypes = [dbl, u32, dbl, dbl]
+        for nm in ("or_uv_counts_f64", "or_uv_counts_f32"):
+            getattr(lib, nm).restype = u64
+            getattr(lib, nm).argtypes = [vp, C.c_size_t, u32, vp, vp]
+        lib.or_chi2_statistic.restype = dbl
+        lib.or_chi2_statistic.argtypes = [vp, u32]
+        lib.or_chi2_sf.restype = dbl
+        lib.or_chi2_sf.argtypes = [dbl, u32]
+        for nm in ("or_autocorr_f64", "or_autocorr_f32"):
+            getattr(lib, nm).restype = dbl
+            getattr(lib, nm).argtypes = [vp, C.c_size_t, C.c_size_t]
         _oracle_lib = lib
     return _oracle_lib
 
@@ -158,6 +171,9 @@ def ref_lib():
         lib.ref_regenerate.argtypes = [u32, vp, vp, vp, vp, C.POINTER(Params),
                                        C.POINTER(dbl), C.POINTER(dbl)]
         lib.ref_moments.argtypes = [vp, C.c_size_t, vp]
+        lib.ref_uv_chi2.argtypes = [vp, C.c_size_t, u32, vp]
+        lib.ref_chi2_sf.argtypes = [dbl, u32, C.POINTER(dbl)]
+        lib.ref_autocorr.argtypes = [vp, C.c_size_t, C.c_size_t, C.POINTER(dbl)]
         lib.ref_state_create.argtypes = [u32, u32, u8, u64, u64, u64, u64, C.POINTER(vp)]
         lib.ref_state_destroy.argtypes = [vp]
         lib.ref_state_fill.argtypes = [vp, vp, C.c_size_t, dbl, dbl]
@@ -310,6 +326,56 @@ def anderson_darling(v: np.ndarray) -> float:
     v = np.ascontiguousarray(v)
     fn = lib.or_anderson_darling_f64 if v.dtype == np.float64 else lib.or_anderson_darling_f32
     return float(fn(v.ctypes.data, v.size))
+
+
+def uv_counts(v: np.ndarray, k: int):
+    """Pairs (v[2i], v[2i+1]) -> to_uv -> k-bin counts of u and v
+    (stats.cpp:10-38 as tools/main.cpp:160-193 uses them)."""
+    lib = oracle_lib()
+    v = np.ascontiguousarray(v)
+    cu = np.zeros(k, dtype=np.uint64)
+    cv = np.zeros(k, dtype=np.uint64)
+    fn = lib.or_uv_counts_f64 if v.dtype == np.float64 else lib.or_uv_counts_f32
+    skipped = int(fn(v.ctypes.data, v.size, k, cu.ctypes.data, cv.ctypes.data))
+    return cu, cv, skipped
+
+
+def chi2_statistic(counts: np.ndarray) -> float:
+    c = np.ascontiguousarray(counts, dtype=np.uint64)
+    return float(oracle_lib().or_chi2_statistic(c.ctypes.data, c.size))
+
+
+def chi2_sf(statistic: float, dof: int) -> float:
+    return float(oracle_lib().or_chi2_sf(statistic, dof))
+
+
+def autocorr(v: np.ndarray, lag: int) -> float:
+    lib = oracle_lib()
+    v = np.ascontiguousarray(v)
+    fn = lib.or_autocorr_f64 if v.dtype == np.float64 else lib.or_autocorr_f32
+    return float(fn(v.ctypes.data, v.size, lag))
+
+
+def ref_uv_chi2(v: np.ndarray, k: int) -> dict:
+    """The reference's own to_uv + chi2_bins on float64 values."""
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    out = np.zeros(6, dtype=np.float64)
+    _check(ref_lib().ref_uv_chi2(v.ctypes.data, v.size, k, out.ctypes.data), "ref_uv_chi2")
+    return {"u_statistic": out[0], "u_p": out[1], "v_statistic": out[2], "v_p": out[3],
+            "samples": int(out[4]), "dof": int(out[5])}
+
+
+def ref_chi2_sf(statistic: float, dof: int) -> float:
+    r = C.c_double()
+    _check(ref_lib().ref_chi2_sf(statistic, dof, C.byref(r)), "ref_chi2_sf")
+    return r.value
+
+
+def ref_autocorr(v: np.ndarray, lag: int) -> float:
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    r = C.c_double()
+    _check(ref_lib().ref_autocorr(v.ctypes.data, v.size, lag, C.byref(r)), "ref_autocorr")
+    return r.value
 
 
 class RefUniform:

@@ -184,6 +184,36 @@ int ref_moments(const double* v, size_t n, double* out7) {
     });
 }
 
+// ---- uniformity / serial-correlation checks (stats.cpp:10-38, 40-127) ----
+// u/v chi-squared exactly as the CLI's uniformity test builds it
+// (tools/main.cpp:160-193): pairs (v[2i], v[2i+1]), to_uv, chi2_bins.
+int ref_uv_chi2(const double* v, size_t n, uint32_t k, double* out6) {
+    return guarded([&] {
+        constexpr double kPi2 = 1.5707963267948966;
+        std::vector<double> us, vs;
+        for (size_t i = 0; i + 1 < n; i += 2) {
+            UvPair q = to_uv(v[i], v[i + 1]);
+            if (q.skip) continue;
+            us.push_back(q.u);
+            vs.push_back(q.v);
+        }
+        Chi2Report a = chi2_bins(us, k, 0.0, 1.0);
+        Chi2Report b = chi2_bins(vs, k, -kPi2, kPi2);
+        out6[0] = a.statistic;
+        out6[1] = a.p_value;
+        out6[2] = b.statistic;
+        out6[3] = b.p_value;
+        out6[4] = double(a.sample_count);
+        out6[5] = double(a.dof);
+    });
+}
+int ref_chi2_sf(double statistic, uint32_t dof, double* out) {
+    return guarded([&] { *out = chi2_sf(statistic, dof); });
+}
+int ref_autocorr(const double* v, size_t n, size_t lag, double* out) {
+    return guarded([&] { *out = autocorr_at_lag(std::span<const double>(v, n), lag).r; });
+}
+
 // ---- WallaceState (wallace.hpp:113-174) --------------------------------
 int ref_state_create(uint32_t pool_exponent, uint32_t f, uint8_t mode,
                      uint64_t restart, uint64_t drift, uint64_t seed,

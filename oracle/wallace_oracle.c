@@ -606,3 +606,127 @@ double or_anderson_darling_f32(const float* v, size_t n) {
     free(z);
     return a;
 }
+
+/* ------------------------------------------------------------------------
+ * Uniformity / serial-correlation checks (restated from stats.cpp:10-38,
+ * 40-87 and 110-127; pairing as tools/main.cpp:160-193).
+ * ---------------------------------------------------------------------- */
+int or_to_uv(double x, double y, double* u, double* v) {
+    /* stats.cpp:10-16 */
+    if (x == 0.0 && y == 0.0) {
+        *u = 0.0;
+        *v = 0.0;
+        return 1;
+    }
+    *u = exp(-0.5 * (x * x + y * y));
+    *v = y == 0.0 ? copysign(1.5707963267948966, x) : atan(x / y);
+    return 0;
+}
+
+int64_t or_chi2_bin(double v, uint32_t k, double lo, double hi) {
+    /* stats.cpp:24-29 */
+    if (!(v >= lo && v <= hi)) return -1;
+    const double width = hi - lo;
+    uint32_t bin = (uint32_t)((v - lo) / width * k);
+    if (bin >= k) bin = k - 1;
+    return (int64_t)bin;
+}
+
+static uint64_t uv_counts(const double* vd, const float* vf, size_t n, uint32_t k, uint64_t* cu,
+                          uint64_t* cv) {
+    const double kPi2 = 1.5707963267948966; /* tools/main.cpp:162 */
+    uint64_t skipped = 0;
+    memset(cu, 0, k * sizeof(uint64_t));
+    memset(cv, 0, k * sizeof(uint64_t));
+    for (size_t i = 0; i + 1 < n; i += 2) {
+        const double x = vd ? vd[i] : (double)vf[i];
+        const double y = vd ? vd[i + 1] : (double)vf[i + 1];
+        double u, v;
+        if (or_to_uv(x, y, &u, &v)) {
+            ++skipped;
+            continue;
+        }
+        ++cu[or_chi2_bin(u, k, 0.0, 1.0)];
+        ++cv[or_chi2_bin(v, k, -kPi2, kPi2)];
+    }
+    return skipped;
+}
+
+uint64_t or_uv_counts_f64(const double* v, size_t n, uint32_t k, uint64_t* cu, uint64_t* cv) {
+    return uv_counts(v, NULL, n, k, cu, cv);
+}
+
+uint64_t or_uv_counts_f32(const float* v, size_t n, uint32_t k, uint64_t* cu, uint64_t* cv) {
+    return uv_counts(NULL, v, n, k, cu, cv);
+}
+
+double or_chi2_statistic(const uint64_t* counts, uint32_t k) {
+    /* stats.cpp:30-35 */
+    uint64_t total = 0;
+    for (uint32_t i = 0; i < k; ++i) total += counts[i];
+    const double expected = (double)total / k;
+    double statistic = 0.0;
+    for (uint32_t i = 0; i < k; ++i) {
+        const double d = (double)counts[i] - expected;
+        statistic += d * d / expected;
+    }
+    return statistic;
+}
+
+static double gamma_p_series(double a, double x) {
+    /* stats.cpp:44-55 */
+    double ap = a, term = 1.0 / a, sum = term;
+    for (int i = 0; i < 100000; ++i) {
+        ap += 1.0;
+        term *= x / ap;
+        sum += term;
+        if (fabs(term) < fabs(sum) * 1e-16) break;
+    }
+    return sum * exp(-x + a * log(x) - lgamma(a));
+}
+
+static double gamma_q_contfrac(double a, double x) {
+    /* stats.cpp:57-75 (modified Lentz) */
+    const double tiny = 1e-300;
+    double b = x + 1.0 - a, c = 1.0 / tiny, d = 1.0 / b, h = d;
+    for (int i = 1; i < 100000; ++i) {
+        const double an = -i * (i - a);
+        b += 2.0;
+        d = an * d + b;
+        if (fabs(d) < tiny) d = tiny;
+        c = b + an / c;
+        if (fabs(c) < tiny) c = tiny;
+        d = 1.0 / d;
+        const double del = d * c;
+        h *= del;
+        if (fabs(del - 1.0) < 1e-16) break;
+    }
+    return h * exp(-x + a * log(x) - lgamma(a));
+}
+
+double or_chi2_sf(double statistic, uint32_t dof) {
+    /* stats.cpp:79-87 */
+    if (statistic < 0.0 || dof < 1) return NAN;
+    if (statistic == 0.0) return 1.0;
+    const double a = 0.5 * dof, x = 0.5 * statistic;
+    return x < a + 1.0 ? 1.0 - gamma_p_series(a, x) : gamma_q_contfrac(a, x);
+}
+
+static double autocorr(const double* vd, const float* vf, size_t n, size_t lag) {
+    /* stats.cpp:110-127 */
+    if (n < lag + 2) return NAN;
+    double mean = 0.0;
+    for (size_t i = 0; i < n; ++i) mean += vd ? vd[i] : (double)vf[i];
+    mean /= (double)n;
+    const size_t pairs = n - lag;
+    double num = 0.0, den = 0.0;
+    for (size_t t = 0; t < pairs; ++t) {
+        const double a = (vd ? vd[t] : (double)vf[t]) - mean;
+        num += a * ((vd ? vd[t + lag] : (double)vf[t + lag]) - mean);
+        den += a * a;
+    }
+    return den == 0.0 ? NAN : num / den;
+}
+
+double or_autocorr_f64(const double* v, size_t n, size_t lag) { return autocorr(v, NULL, n, lag); }
+double or_autocorr_f32(const float* v, size_t n, size_t lag) { return autocorr(NULL, v, n, lag); }

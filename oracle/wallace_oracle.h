@@ -129,6 +129,26 @@ void or_moments_f32(const float* v, size_t n, double* out5);
 double or_anderson_darling_f64(const double* v, size_t n);
 double or_anderson_darling_f32(const float* v, size_t n);
 
+/* ---- uniformity and serial-correlation checks (stats.cpp:10-38, 110-127;
+ * the CLI's pairing, tools/main.cpp:160-193) ---- */
+/* to_uv: u = exp(-(x^2 + y^2)/2), v = atan(x / y) (y == 0: copysign(pi/2, x));
+ * returns 1 (skip) for the (0, 0) pair. */
+int or_to_uv(double x, double y, double* u, double* v);
+/* chi2_bins' bin index of v in [lo, hi] with k bins (values == hi -> k - 1);
+ * -1 when v is outside [lo, hi]. */
+int64_t or_chi2_bin(double v, uint32_t k, double lo, double hi);
+/* Pairs (v[2i], v[2i+1]), i < n/2, mapped by to_uv; u binned on [0, 1] and
+ * v on [-pi/2, pi/2] into k bins each.  Returns the skipped-pair count. */
+uint64_t or_uv_counts_f64(const double* v, size_t n, uint32_t k, uint64_t* cu, uint64_t* cv);
+uint64_t or_uv_counts_f32(const float* v, size_t n, uint32_t k, uint64_t* cu, uint64_t* cv);
+/* chi2_bins' statistic from counts (expected = total / k, summed in bin order). */
+double or_chi2_statistic(const uint64_t* counts, uint32_t k);
+/* chi2_sf (stats.cpp:40-87): regularized upper incomplete gamma. */
+double or_chi2_sf(double statistic, uint32_t dof);
+/* autocorr_at_lag (stats.cpp:110-127): r, two-pass, sequential sums. */
+double or_autocorr_f64(const double* v, size_t n, size_t lag);
+double or_autocorr_f32(const float* v, size_t n, size_t lag);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,12 +16,16 @@ from .wallace import (  # noqa: F401
     StateErrorKind,
     WallaceConfig,
     WallaceState,
+    chi2_sf,
+    device_autocorr,
     device_moments,
+    device_uv_chi2,
     lfg_words,
+    validate,
 )
 
 __all__ = [
     "CorruptedStateError", "CudaError", "MalformedStateError", "PassParams", "Pool",
     "Rotation2", "ScaleMode", "StateErrorKind", "WallaceConfig", "WallaceState",
-    "device_moments", "lfg_words",
+    "device_moments", "lfg_words", "device_uv_chi2", "device_autocorr", "chi2_sf", "validate",
 ]

@@ -71,6 +71,20 @@ class Counters(C.Structure):
     ]
 
 
+class Validation(C.Structure):  # wrng_gpu_validation
+    _fields_ = [
+        ("n", C.c_uint64),
+        ("m1", C.c_double), ("m2", C.c_double), ("m3", C.c_double), ("m4", C.c_double),
+        ("z1", C.c_double), ("z2", C.c_double), ("z4", C.c_double),
+        ("uv_samples", C.c_uint64), ("uv_skipped", C.c_uint64),
+        ("k", C.c_uint32), ("dof", C.c_uint32),
+        ("u_statistic", C.c_double), ("u_p", C.c_double),
+        ("v_statistic", C.c_double), ("v_p", C.c_double),
+        ("lag", C.c_uint64),
+        ("autocorr", C.c_double),
+    ]
+
+
 # Every symbol include/wrng_gpu.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "wrng_gpu_config_default", "wrng_gpu_create", "wrng_gpu_destroy",
@@ -80,7 +94,8 @@ EXPORTS = (
     "wrng_gpu_write_pool", "wrng_gpu_read_uniform", "wrng_gpu_export_state",
     "wrng_gpu_import_state", "wrng_gpu_synchronize", "wrng_gpu_last_error",
     "wrng_gpu_kernel_launches", "wrng_gpu_engine", "wrng_gpu_moments_f32",
-    "wrng_gpu_moments_f64", "wrng_gpu_lfg_words",
+    "wrng_gpu_moments_f64", "wrng_gpu_lfg_words", "wrng_gpu_uv_counts", "wrng_gpu_autocorr",
+    "wrng_gpu_chi2_sf", "wrng_gpu_validate",
 )
 
 
@@ -116,6 +131,10 @@ def _load():
         "wrng_gpu_moments_f32": (C.c_int, [vp, u64, vp, i32, vp]),
         "wrng_gpu_moments_f64": (C.c_int, [vp, u64, vp, i32, vp]),
         "wrng_gpu_lfg_words": (C.c_int, [u64, u64, u32, u64, vp, i32]),
+        "wrng_gpu_uv_counts": (C.c_int, [vp, i32, u64, u32, vp, vp, P(u64), i32, vp]),
+        "wrng_gpu_autocorr": (C.c_int, [vp, i32, u64, u64, P(dbl), i32, vp]),
+        "wrng_gpu_chi2_sf": (dbl, [dbl, u32]),
+        "wrng_gpu_validate": (C.c_int, [vp, u64, u32, u64, vp, vp, P(Validation)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -1183,6 +1183,242 @@ wrng_gpu_status wrng_gpu_moments_f64(const double* dev, uint64_t n, double* out5
     return moments_any(dev, 0, n, out5, device, stream);
 }
 
+// ---- validation statistics -----------------------------
+}  // extern "C"
+
+namespace {
+
+// chi2_sf (stats.cpp:40-87): regularized upper incomplete gamma, series /
+// continued fraction split at x = a + 1.
+double gamma_p_series(double a, double x) {
+    double ap = a, term = 1.0 / a, sum = term;
+    for (int i = 0; i < 100000; ++i) {
+        ap += 1.0;
+        term *= x / ap;
+        sum += term;
+        if (std::fabs(term) < std::fabs(sum) * 1e-16) break;
+    }
+    return sum * std::exp(-x + a * std::log(x) - std::lgamma(a));
+}
+
+double gamma_q_contfrac(double a, double x) {
+    const double tiny = 1e-300;
+    double b = x + 1.0 - a, c = 1.0 / tiny, d = 1.0 / b, h = d;
+    for (int i = 1; i < 100000; ++i) {
+        const double an = -i * (i - a);
+        b += 2.0;
+        d = an * d + b;
+        if (std::fabs(d) < tiny) d = tiny;
+        c = b + an / c;
+        if (std::fabs(c) < tiny) c = tiny;
+        d = 1.0 / d;
+        const double del = d * c;
+        h *= del;
+        if (std::fabs(del - 1.0) < 1e-16) break;
+    }
+    return h * std::exp(-x + a * std::log(x) - std::lgamma(a));
+}
+
+// chi2_bins' statistic (stats.cpp:30-35): expected = total / k, bin order.
+double chi2_statistic(const std::vector<uint64_t>& c, uint64_t total) {
+    const double expected = (double)total / (double)c.size();
+    double st = 0.0;
+    for (uint64_t x : c) {
+        const double d = (double)x - expected;
+        st += d * d / expected;
+    }
+    return st;
+}
+
+// Device scratch of one statistics call.
+struct StatBufs {
+    wrng_gpu* g = nullptr;
+    double* part = nullptr;           // per-block partials (4 per block)
+    double* acc = nullptr;            // [0..3] moment sums, [4..7] lag sums
+    unsigned long long* cnt = nullptr;  // [k] u, [k] v, [1] skipped
+    void* tail[2] = {nullptr, nullptr};
+    static constexpr uint32_t kBlocks = 148 * 4;
+    ~StatBufs() {
+        cudaFree(part);
+        cudaFree(acc);
+        cudaFree(cnt);
+        cudaFree(tail[0]);
+        cudaFree(tail[1]);
+    }
+    cudaError_t init(uint32_t k, size_t tail_bytes, cudaStream_t s) {
+        cudaError_t e = cudaMalloc(&part, sizeof(double) * 4 * kBlocks);
+        if (e == cudaSuccess) e = cudaMalloc(&acc, sizeof(double) * 8);
+        if (e == cudaSuccess) e = cudaMalloc(&cnt, sizeof(unsigned long long) * (2 * k + 1));
+        if (e == cudaSuccess && tail_bytes) e = cudaMalloc(&tail[0], tail_bytes);
+        if (e == cudaSuccess && tail_bytes) e = cudaMalloc(&tail[1], tail_bytes);
+        if (e == cudaSuccess) e = cudaMemsetAsync(acc, 0, sizeof(double) * 8, s);
+        if (e == cudaSuccess)
+            e = cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (2 * k + 1), s);
+        return e;
+    }
+};
+
+double autocorr_from_sums(const double* acc, uint64_t n, uint64_t pairs) {
+    const double m = acc[0] / (double)n, P = (double)pairs;
+    const double num = acc[4] - m * (acc[5] + acc[6]) + P * m * m;
+    const double den = acc[7] - 2.0 * m * acc[5] + P * m * m;
+    return den == 0.0 ? NAN : num / den;
+}
+
+}  // namespace
+
+extern "C" {
+
+double wrng_gpu_chi2_sf(double statistic, uint32_t dof) {
+    if (statistic < 0.0 || dof < 1) return NAN;
+    if (statistic == 0.0) return 1.0;
+    const double a = 0.5 * dof, x = 0.5 * statistic;
+    return x < a + 1.0 ? 1.0 - gamma_p_series(a, x) : gamma_q_contfrac(a, x);
+}
+
+wrng_gpu_status wrng_gpu_uv_counts(const void* dev, int32_t is_f32, uint64_t n, uint32_t k,
+                                   uint64_t* counts_u, uint64_t* counts_v, uint64_t* skipped,
+                                   int32_t device, void* stream) {
+    if (!dev || !counts_u || !counts_v || k < 2 || k > 8192) return WRNG_GPU_EINVAL;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return WRNG_GPU_ENODEV;
+    DeviceGuard dg(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    StatBufs b;
+    cudaError_t e = b.init(k, 0, s);
+    if (e == cudaSuccess)
+        e = launch_uv_counts(dev, is_f32, 1, n, n, k, b.cnt, b.cnt + k, b.cnt + 2 * k, s);
+    std::vector<unsigned long long> h(2 * k + 1);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(h.data(), b.cnt, sizeof(unsigned long long) * h.size(),
+                       cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return WRNG_GPU_ECUDA;
+    for (uint32_t i = 0; i < k; ++i) {
+        counts_u[i] = h[i];
+        counts_v[i] = h[k + i];
+    }
+    if (skipped) *skipped = h[2 * k];
+    return WRNG_GPU_OK;
+}
+
+wrng_gpu_status wrng_gpu_autocorr(const void* dev, int32_t is_f32, uint64_t n, uint64_t lag,
+                                  double* r, int32_t device, void* stream) {
+    if (!dev || !r || n < lag + 2) return WRNG_GPU_EINVAL;  // stats.cpp:112-113
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return WRNG_GPU_ENODEV;
+    DeviceGuard dg(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    StatBufs b;
+    cudaError_t e = b.init(2, 0, s);
+    if (e == cudaSuccess)
+        e = launch_moment_sums(dev, is_f32, 1, n, n, b.part, StatBufs::kBlocks, b.acc, s);
+    if (e == cudaSuccess)
+        e = launch_ac_sums(dev, dev, is_f32, 1, n, n, lag, 0, b.part, StatBufs::kBlocks,
+                           b.acc + 4, s);
+    double acc[8];
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaMemcpy(acc, b.acc, sizeof(acc), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return WRNG_GPU_ECUDA;
+    *r = autocorr_from_sums(acc, n, n - lag);
+    return WRNG_GPU_OK;
+}
+
+wrng_gpu_status wrng_gpu_validate(wrng_gpu_t* g, uint64_t count, uint32_t k, uint64_t lag,
+                                  uint64_t* counts_u, uint64_t* counts_v,
+                                  wrng_gpu_validation* out) {
+    if (!g || !out || k < 2 || k > 8192) return WRNG_GPU_EINVAL;
+    DeviceGuard dg(g->cfg.device);
+    wrng_gpu_status st = ensure_stage(g);
+    if (st) return st;
+    const uint32_t P = g->cfg.pools;
+    const int f32 = g->cfg.dtype == WRNG_GPU_F32;
+    const size_t esz = f32 ? 4 : 8;
+    const uint64_t base = count / P, extra = count % P;
+    cudaStream_t s = g->stream;
+    StatBufs b;
+    CK(b.init(k, (size_t)P * lag * esz, s));
+    // windows of L values per pool (even: pairs never straddle windows), the
+    // slab kept <= 64 MiB so the reductions re-read it from L2
+    const uint64_t slab = std::min<uint64_t>(g->stage_bytes, (uint64_t)64 << 20) / esz;
+    const uint64_t L = std::max<uint64_t>(2, (slab / P) & ~1ull);
+    uint64_t have = 0;
+    int cur = 0;
+    for (uint64_t t = 0;; t += L) {
+        const bool tail = t + L > base;
+        OutLayout lay{};
+        lay.off_stride = L;
+        lay.len_base = tail ? base - t : L;
+        lay.len_extra = tail ? extra : 0;
+        if (lay.len_base == 0 && lay.len_extra == 0) break;
+        st = fill_device(g, g->stage[0], f32, lay, 0.0, 1.0, s);
+        if (st) return st;
+        // groups of equal window length: [0, len_extra) one longer
+        struct Grp {
+            uint32_t p0, np;
+            uint64_t len;
+        } grp[2] = {{0, (uint32_t)lay.len_extra, lay.len_base + 1},
+                    {(uint32_t)lay.len_extra, P - (uint32_t)lay.len_extra, lay.len_base}};
+        for (const Grp& gr : grp) {
+            if (gr.np == 0 || gr.len == 0) continue;
+            const char* w = static_cast<const char*>(g->stage[0]) + (size_t)gr.p0 * L * esz;
+            CK(launch_moment_sums(w, f32, gr.np, L, gr.len, b.part, StatBufs::kBlocks, b.acc, s));
+            CK(launch_uv_counts(w, f32, gr.np, L, gr.len, k, b.cnt, b.cnt + k, b.cnt + 2 * k, s));
+            if (lag) {
+                const size_t to = (size_t)gr.p0 * lag * esz;
+                const char* told = static_cast<const char*>(b.tail[cur]) + to;
+                char* tnew = static_cast<char*>(b.tail[cur ^ 1]) + to;
+                CK(launch_ac_sums(w, told, f32, gr.np, L, gr.len, lag, have, b.part,
+                                  StatBufs::kBlocks, b.acc + 4, s));
+                CK(launch_ac_tail(w, told, tnew, f32, gr.np, L, gr.len, lag, have, s));
+            }
+            g->launches += lag ? 6 : 4;
+        }
+        cur ^= 1;
+        have = std::min<uint64_t>(lag, have + lay.len_base);
+        if (tail) break;
+    }
+    double acc[8];
+    std::vector<unsigned long long> h(2 * k + 1);
+    CK(cudaStreamSynchronize(s));
+    CK(cudaMemcpy(acc, b.acc, sizeof(acc), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(h.data(), b.cnt, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
+    st = collect(g);
+    if (st) return st;
+    wrng_gpu_validation v{};
+    v.n = count;
+    const double dn = (double)count;
+    v.m1 = acc[0] / dn;
+    v.m2 = acc[1] / dn;
+    v.m3 = acc[2] / dn;
+    v.m4 = acc[3] / dn;
+    v.z1 = v.m1 * std::sqrt(dn / 1.0);  // stats.cpp:103-105
+    v.z2 = (v.m2 - 1.0) * std::sqrt(dn / 2.0);
+    v.z4 = (v.m4 - 3.0) * std::sqrt(dn / 96.0);
+    std::vector<uint64_t> cu(h.begin(), h.begin() + k), cv(h.begin() + k, h.begin() + 2 * k);
+    for (uint64_t x : cu) v.uv_samples += x;
+    v.uv_skipped = h[2 * k];
+    v.k = k;
+    v.dof = k - 1;
+    if (v.uv_samples) {
+        v.u_statistic = chi2_statistic(cu, v.uv_samples);
+        v.v_statistic = chi2_statistic(cv, v.uv_samples);
+        v.u_p = wrng_gpu_chi2_sf(v.u_statistic, v.dof);
+        v.v_p = wrng_gpu_chi2_sf(v.v_statistic, v.dof);
+    }
+    v.lag = lag;
+    uint64_t pairs = 0;
+    for (uint32_t p = 0; p < P; ++p) {
+        const uint64_t np = base + (p < extra ? 1 : 0);
+        pairs += np > lag ? np - lag : 0;
+    }
+    v.autocorr = lag && pairs ? autocorr_from_sums(acc, count, pairs) : NAN;
+    if (counts_u) std::copy(cu.begin(), cu.end(), counts_u);
+    if (counts_v) std::copy(cv.begin(), cv.end(), counts_v);
+    *out = v;
+    return WRNG_GPU_OK;
+}
+
 wrng_gpu_status wrng_gpu_lfg_words(uint64_t seed, uint64_t stream_id, uint32_t pools,
                                    uint64_t count, uint64_t* host_out, int32_t device) {
     if (!host_out || pools == 0) return WRNG_GPU_EINVAL;

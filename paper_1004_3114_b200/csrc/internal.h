@@ -148,6 +148,21 @@ cudaError_t launch_hbm_setmeta(PoolMeta* meta, uint64_t pass_count, uint64_t ava
 cudaError_t launch_moments(const void* v, int is_f32, uint64_t n, double* partials,
                            uint32_t nblocks, double* out5_dev, cudaStream_t st);
 
+// Uniformity / serial-correlation checks on P stream windows (misc.cu).
+cudaError_t launch_uv_counts(const void* v, int is_f32, uint32_t P, uint64_t pitch,
+                             uint64_t len, uint32_t k, unsigned long long* cu,
+                             unsigned long long* cv, unsigned long long* skipped,
+                             cudaStream_t st);
+cudaError_t launch_ac_sums(const void* v, const void* tail, int is_f32, uint32_t P,
+                           uint64_t pitch, uint64_t len, uint64_t lag, uint64_t have,
+                           double* part, uint32_t nb, double* acc, cudaStream_t st);
+cudaError_t launch_moment_sums(const void* v, int is_f32, uint32_t P, uint64_t pitch,
+                               uint64_t len, double* part, uint32_t nb, double* acc,
+                               cudaStream_t st);
+cudaError_t launch_ac_tail(const void* v, const void* told, void* tnew, int is_f32, uint32_t P,
+                           uint64_t pitch, uint64_t len, uint64_t lag, uint64_t have,
+                           cudaStream_t st);
+
 // Device uniform generator words (tests).
 cudaError_t launch_lfg_words(uint64_t seed, uint64_t stream0, uint32_t pools,
                              uint64_t count, uint64_t* out, cudaStream_t st);

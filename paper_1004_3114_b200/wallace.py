@@ -365,3 +365,69 @@ def lfg_words(seed: int, stream_id: int, pools: int, count: int, device: int = 0
     _raise(lib.wrng_gpu_lfg_words(seed, stream_id, pools, count, out.ctypes.data, device),
            "lfg_words")
     return out
+
+
+# ---- validation statistics on the device ---------------
+def _dev_args(t, stream):
+    import torch
+
+    if not (t.is_cuda and t.is_contiguous()) or t.dtype not in (torch.float32, torch.float64):
+        raise ValueError("expected a contiguous float32/float64 CUDA tensor")
+    if stream is None:
+        stream = torch.cuda.current_stream(t.device)
+    return t.data_ptr(), 1 if t.dtype == torch.float32 else 0, t.device.index or 0, \
+        stream.cuda_stream
+
+
+def chi2_sf(statistic: float, dof: int) -> float:
+    """Survival function of chi-squared(dof) (stats.cpp:40-87)."""
+    return float(lib.wrng_gpu_chi2_sf(statistic, dof))
+
+
+def _chi2_report(counts: np.ndarray) -> dict:
+    total = int(counts.sum())
+    k = counts.size
+    expected = total / k
+    stat = 0.0
+    for c in counts.tolist():  # bin order, as chi2_bins sums (stats.cpp:30-35)
+        d = float(c) - expected
+        stat += d * d / expected
+    return {"statistic": stat, "dof": k - 1, "p_value": chi2_sf(stat, k - 1), "bin_count": k,
+            "sample_count": total}
+
+
+def device_uv_chi2(t, k: int = 1000, stream=None) -> dict:
+    """u/v uniformity of a CUDA tensor of normals, paired (2i, 2i+1) as the
+    reference CLI's uniformity test (tools/main.cpp:160-193; stats.cpp:10-38):
+    {"u": Chi2Report, "v": Chi2Report, "skipped": pairs (0, 0), "counts_u",
+    "counts_v"}."""
+    ptr, f32, dev, st = _dev_args(t, stream)
+    cu = np.zeros(k, dtype=np.uint64)
+    cv = np.zeros(k, dtype=np.uint64)
+    sk = C.c_uint64()
+    _raise(lib.wrng_gpu_uv_counts(ptr, f32, t.numel(), k, cu.ctypes.data, cv.ctypes.data,
+                                  C.byref(sk), dev, st), "uv_counts")
+    return {"u": _chi2_report(cu), "v": _chi2_report(cv), "skipped": int(sk.value),
+            "counts_u": cu, "counts_v": cv}
+
+
+def device_autocorr(t, lag: int, stream=None) -> float:
+    """autocorr_at_lag(t, lag).r (stats.cpp:110-127) on the device."""
+    ptr, f32, dev, st = _dev_args(t, stream)
+    r = C.c_double()
+    _raise(lib.wrng_gpu_autocorr(ptr, f32, t.numel(), lag, C.byref(r), dev, st), "autocorr")
+    return r.value
+
+
+def validate(state: "WallaceState", count: int, k: int = 1000, lag: int = 1) -> dict:
+    """Generate `count` values of `state` (advancing it exactly like
+    state.fill(count)) and check them on the device: moments with z-scores,
+    u/v chi-squared, autocorrelation at `lag`.  No values reach the host."""
+    v = L.Validation()
+    cu = np.zeros(k, dtype=np.uint64)
+    cv = np.zeros(k, dtype=np.uint64)
+    _raise(lib.wrng_gpu_validate(state._h, count, k, lag, cu.ctypes.data, cv.ctypes.data,
+                                 C.byref(v)), "validate", state._h)
+    out = {f: getattr(v, f) for f, _ in L.Validation._fields_}
+    out["counts_u"], out["counts_v"] = cu, cv
+    return out
