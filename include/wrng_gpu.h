@@ -227,6 +227,19 @@ wrng_gpu_status wrng_gpu_validate(wrng_gpu_t* g, uint64_t count, uint32_t k, uin
                                   uint64_t* counts_u, uint64_t* counts_v,
                                   wrng_gpu_validation* out);
 
+/* ---- Box-Muller / polar baselines (reference.cpp:9-63) --
+ * The methods the paper compares Wallace against, on the
+ * GPU: stream p = UniformState(seed, stream_id + p) fills count / pools
+ * values (+1 for p < count % pools) as a FRESH box_muller_fill (method 0)
+ * or polar_fill (method 1) would, pool-major into DEVICE memory, on
+ * `stream` (asynchronous).  f64_math = 1 evaluates the reference's fp64
+ * expressions (CUDA libm: within a few ulp of glibc); 0 uses fp32 math
+ * (logf, sqrtf, sincospif) as a throughput baseline. */
+wrng_gpu_status wrng_gpu_method_fill(int32_t method, uint64_t seed, uint64_t stream_id,
+                                     uint32_t pools, void* dev_out, int32_t out_f32,
+                                     uint64_t count, double mu, double sigma, int32_t f64_math,
+                                     int32_t device, void* stream);
+
 /* Device uniform generator, for bit-exact stream checks: the first `count`
  * next_word() outputs of UniformState(seed, stream_id + p) for p < pools,
  * pool-major (uniform.cpp:23-40). */

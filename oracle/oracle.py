@@ -123,6 +123,7 @@ def oracle_lib():
         lib.or_anderson_darling_f64.argtypes = [vp, C.c_size_t]
         lib.or_anderson_darling_f32.restype = dbl
         lib.or_anderson_darling_f32.argtypes = [vp, C.c_size_t]
+        lib.or_method_bank_fill.argtypes = [C.c_int, u64, u64, u32, u64, vp]
         lib.or_to_uv.argtypes = [dbl, dbl, C.POINTER(dbl), C.POINTER(dbl)]
         lib.or_chi2_bin.restype = C.c_int64
         lib.or_chi2_bin.argtypes = [dbl, u32, dbl, dbl]
@@ -171,6 +172,9 @@ def ref_lib():
         lib.ref_regenerate.argtypes = [u32, vp, vp, vp, vp, C.POINTER(Params),
                                        C.POINTER(dbl), C.POINTER(dbl)]
         lib.ref_moments.argtypes = [vp, C.c_size_t, vp]
+        lib.ref_polar_fill.argtypes = [vp, vp, C.c_size_t, dbl, dbl]
+        lib.ref_bench_methods.restype = dbl
+        lib.ref_bench_methods.argtypes = [C.c_int, u32, u64, u64]
         lib.ref_uv_chi2.argtypes = [vp, C.c_size_t, u32, vp]
         lib.ref_chi2_sf.argtypes = [dbl, u32, C.POINTER(dbl)]
         lib.ref_autocorr.argtypes = [vp, C.c_size_t, C.c_size_t, C.POINTER(dbl)]
@@ -328,6 +332,15 @@ def anderson_darling(v: np.ndarray) -> float:
     return float(fn(v.ctypes.data, v.size))
 
 
+def method_bank_fill(method: str, seed: int, stream0: int, pools: int, count: int) -> np.ndarray:
+    """Box-Muller ("boxmuller") or polar ("polar") fills of `pools` fresh
+    UniformState(seed, stream0 + p) streams, pool-major (reference.cpp:41-63)."""
+    out = np.empty(count, dtype=np.float64)
+    oracle_lib().or_method_bank_fill(0 if method == "boxmuller" else 1, seed, stream0, pools,
+                                     count, out.ctypes.data)
+    return out
+
+
 def uv_counts(v: np.ndarray, k: int):
     """Pairs (v[2i], v[2i+1]) -> to_uv -> k-bin counts of u and v
     (stats.cpp:10-38 as tools/main.cpp:160-193 uses them)."""
@@ -404,6 +417,23 @@ class RefUniform:
         r, s, d = C.c_uint32(), C.c_uint32(), C.c_uint64()
         self.lib.ref_uniform_get(self.h, t.ctypes.data, C.byref(r), C.byref(s), C.byref(d))
         return t, r.value, s.value, d.value
+
+    def box_muller_fill(self, n: int, mu=0.0, sigma=1.0) -> np.ndarray:
+        out = np.empty(n, dtype=np.float64)
+        self.lib.ref_box_muller_fill(self.h, out.ctypes.data, n, mu, sigma)
+        return out
+
+    def polar_fill(self, n: int, mu=0.0, sigma=1.0) -> np.ndarray:
+        out = np.empty(n, dtype=np.float64)
+        self.lib.ref_polar_fill(self.h, out.ctypes.data, n, mu, sigma)
+        return out
+
+
+def ref_bench_methods(method: str, threads: int, per_thread: int, seed: int = 1) -> float:
+    """Wall seconds for `threads` reference Box-Muller / polar streams of
+    per_thread values each (64Ki-value fill calls)."""
+    return float(ref_lib().ref_bench_methods(0 if method == "boxmuller" else 1, threads,
+                                             per_thread, seed))
 
 
 class RefState:

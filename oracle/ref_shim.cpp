@@ -138,6 +138,31 @@ void ref_box_muller_fill(void* u, double* out, size_t n, double mu, double sigma
     box_muller_fill(*static_cast<UniformState*>(u), std::span<double>(out, n), mu,
                     sigma);
 }
+void ref_polar_fill(void* u, double* out, size_t n, double mu, double sigma) {
+    polar_fill(*static_cast<UniformState*>(u), std::span<double>(out, n), mu, sigma);
+}
+// CPU timing of the reference's non-Wallace methods (main.cpp:287-312 loop):
+// thread t fills per_thread values of UniformState(seed, t) in 64Ki calls.
+double ref_bench_methods(int method, uint32_t threads, uint64_t per_thread, uint64_t seed) {
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> th;
+    for (uint32_t t = 0; t < threads; ++t)
+        th.emplace_back([=] {
+            UniformState us(seed, t);
+            std::vector<double> buf(1u << 16);
+            double sink = 0.0;
+            for (uint64_t done = 0; done < per_thread; done += buf.size()) {
+                if (method == 0)
+                    box_muller_fill(us, buf);
+                else
+                    polar_fill(us, buf);
+                sink += buf[buf.size() / 2];
+            }
+            if (sink == 12345.678) std::abort();
+        });
+    for (auto& x : th) x.join();
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
 // select_pass_params on a caller-described pool (wallace.cpp:51-70).
 int ref_select_pass_params(void* u, uint32_t n, double tracked, double withheld,
                            uint8_t mode, ref_params* out) {

@@ -110,6 +110,57 @@ void or_box_muller_fill(or_uniform* u, double* out, size_t n) {
     }
 }
 
+/* polar_transform / polar_next (reference.cpp:24-39): Marsaglia's polar
+ * method, (v1, v2) = 2u - 1 accepted when 0 < v1^2 + v2^2 < 1. */
+void or_polar_next(or_uniform* u, double* x, double* y) {
+    for (;;) {
+        double v1 = 2.0 * or_next_uniform(u) - 1.0;
+        double v2 = 2.0 * or_next_uniform(u) - 1.0;
+        double s = v1 * v1 + v2 * v2;
+        if (s > 0.0 && s < 1.0) {
+            double f = sqrt(-2.0 * log(s) / s);
+            *x = v1 * f;
+            *y = v2 * f;
+            return;
+        }
+    }
+}
+
+/* polar_fill with mu = 0, sigma = 1 (reference.cpp:46-63). */
+void or_polar_fill(or_uniform* u, double* out, size_t n) {
+    volatile double mu = 0.0, sigma = 1.0;
+    size_t i = 0;
+    double x, y;
+    while (i + 1 < n) {
+        or_polar_next(u, &x, &y);
+        out[i++] = mu + sigma * x;
+        out[i++] = mu + sigma * y;
+    }
+    if (i < n) {
+        or_polar_next(u, &x, &y);
+        out[i] = mu + sigma * x;
+    }
+}
+
+/* Bank of method fills: stream p = UniformState(seed, stream0 + p) fills
+ * count / pools values (+1 for p < count % pools), pool-major; method 0
+ * Box-Muller, 1 polar. */
+void or_method_bank_fill(int method, uint64_t seed, uint64_t stream0, uint32_t pools,
+                         uint64_t count, double* out) {
+    const uint64_t base = count / pools, extra = count % pools;
+    uint64_t off = 0;
+    for (uint32_t p = 0; p < pools; ++p) {
+        const uint64_t len = base + (p < extra ? 1 : 0);
+        or_uniform u;
+        or_uniform_init(&u, seed, stream0 + p);
+        if (method == 0)
+            or_box_muller_fill(&u, out + off, len);
+        else
+            or_polar_fill(&u, out + off, len);
+        off += len;
+    }
+}
+
 /* ------------------------------------------------------------------------
  * Pass parameters (wallace.cpp:27-70) and the n = 4 extension
  * (docs/n4_spec.md §2).

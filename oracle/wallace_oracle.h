@@ -87,6 +87,10 @@ int or_next_int_below(or_uniform* u, uint32_t m, uint32_t* out);
 int or_box_muller_pair(double u1, double u2, double* x, double* y);
 void or_box_muller_next(or_uniform* u, double* x, double* y);
 void or_box_muller_fill(or_uniform* u, double* out, size_t n);
+void or_polar_next(or_uniform* u, double* x, double* y);
+void or_polar_fill(or_uniform* u, double* out, size_t n);
+void or_method_bank_fill(int method, uint64_t seed, uint64_t stream0, uint32_t pools,
+                         uint64_t count, double* out);
 double or_chi2_target(double r, uint32_t nu);
 void or_rotation_from_t(double t, uint32_t region, double* c, double* s);
 int or_select_params(or_uniform* u, uint32_t n_arrays, uint32_t n, double tracked,

@@ -21,6 +21,7 @@ from .wallace import (  # noqa: F401
     device_moments,
     device_uv_chi2,
     lfg_words,
+    method_fill,
     validate,
 )
 
@@ -28,4 +29,5 @@ __all__ = [
     "CorruptedStateError", "CudaError", "MalformedStateError", "PassParams", "Pool",
     "Rotation2", "ScaleMode", "StateErrorKind", "WallaceConfig", "WallaceState",
     "device_moments", "lfg_words", "device_uv_chi2", "device_autocorr", "chi2_sf", "validate",
+    "method_fill",
 ]

@@ -95,7 +95,7 @@ EXPORTS = (
     "wrng_gpu_import_state", "wrng_gpu_synchronize", "wrng_gpu_last_error",
     "wrng_gpu_kernel_launches", "wrng_gpu_engine", "wrng_gpu_moments_f32",
     "wrng_gpu_moments_f64", "wrng_gpu_lfg_words", "wrng_gpu_uv_counts", "wrng_gpu_autocorr",
-    "wrng_gpu_chi2_sf", "wrng_gpu_validate",
+    "wrng_gpu_chi2_sf", "wrng_gpu_validate", "wrng_gpu_method_fill",
 )
 
 
@@ -135,6 +135,8 @@ def _load():
         "wrng_gpu_autocorr": (C.c_int, [vp, i32, u64, u64, P(dbl), i32, vp]),
         "wrng_gpu_chi2_sf": (dbl, [dbl, u32]),
         "wrng_gpu_validate": (C.c_int, [vp, u64, u32, u64, vp, vp, P(Validation)]),
+        "wrng_gpu_method_fill": (C.c_int, [i32, u64, u64, u32, vp, i32, u64, dbl, dbl, i32, i32,
+                                           vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -1419,6 +1419,24 @@ wrng_gpu_status wrng_gpu_validate(wrng_gpu_t* g, uint64_t count, uint32_t k, uin
     return WRNG_GPU_OK;
 }
 
+wrng_gpu_status wrng_gpu_method_fill(int32_t method, uint64_t seed, uint64_t stream_id,
+                                     uint32_t pools, void* dev_out, int32_t out_f32,
+                                     uint64_t count, double mu, double sigma, int32_t f64_math,
+                                     int32_t device, void* stream) {
+    if ((method != 0 && method != 1) || pools == 0 || !(sigma >= 0.0) ||
+        (count > 0 && !dev_out))
+        return WRNG_GPU_EINVAL;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return WRNG_GPU_ENODEV;
+    if (count == 0) return WRNG_GPU_OK;
+    DeviceGuard dg(device);
+    const OutLayout lay{count / pools, count % pools, count / pools, count % pools};
+    cudaError_t e = launch_method_fill(method, f64_math, seed, stream_id, pools, lay, mu, sigma,
+                                       out_f32 ? 1u : 0u, dev_out,
+                                       static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? WRNG_GPU_OK : WRNG_GPU_ECUDA;
+}
+
 wrng_gpu_status wrng_gpu_lfg_words(uint64_t seed, uint64_t stream_id, uint32_t pools,
                                    uint64_t count, uint64_t* host_out, int32_t device) {
     if (!host_out || pools == 0) return WRNG_GPU_EINVAL;

@@ -163,6 +163,11 @@ cudaError_t launch_ac_tail(const void* v, const void* told, void* tnew, int is_f
                            uint64_t pitch, uint64_t len, uint64_t lag, uint64_t have,
                            cudaStream_t st);
 
+// Box-Muller / polar baselines (baselines.cu).
+cudaError_t launch_method_fill(int method, int f64_math, uint64_t seed, uint64_t stream0,
+                               uint32_t pools, const OutLayout& lay, double mu, double sigma,
+                               uint32_t out_f32, void* out, cudaStream_t st);
+
 // Device uniform generator words (tests).
 cudaError_t launch_lfg_words(uint64_t seed, uint64_t stream0, uint32_t pools,
                              uint64_t count, uint64_t* out, cudaStream_t st);

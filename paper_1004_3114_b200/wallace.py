@@ -431,3 +431,16 @@ def validate(state: "WallaceState", count: int, k: int = 1000, lag: int = 1) -> 
     out = {f: getattr(v, f) for f, _ in L.Validation._fields_}
     out["counts_u"], out["counts_v"] = cu, cv
     return out
+
+
+# ---- Box-Muller / polar baselines (reference.cpp:9-63) ----------------------
+def method_fill(method: str, t, seed: int, stream_id: int = 0, pools: int = 1, mu: float = 0.0,
+                sigma: float = 1.0, f64_math: bool = True, stream=None):
+    """Fill the CUDA tensor `t` with `pools` fresh Box-Muller ("boxmuller") or
+    polar ("polar") streams UniformState(seed, stream_id + p), pool-major
+    (asynchronous on `stream`)."""
+    ptr, f32, dev, st = _dev_args(t, stream)
+    m = {"boxmuller": 0, "polar": 1}[method]
+    _raise(lib.wrng_gpu_method_fill(m, seed, stream_id, pools, ptr, f32, t.numel(), mu, sigma,
+                                    1 if f64_math else 0, dev, st), "method_fill")
+    return t
