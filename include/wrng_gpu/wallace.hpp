@@ -212,6 +212,15 @@ public:
     void drift_check() { detail::check(wrng_gpu_drift_check(g_), g_, "drift_check"); }
     void restart() { detail::check(wrng_gpu_restart(g_), g_, "restart"); }
     void synchronize() { detail::check(wrng_gpu_synchronize(g_), g_, "synchronize"); }
+    /// GPU extension: generate `count` values (advancing like fill(count))
+    /// and check them on the device (wrng_gpu_validate).
+    wrng_gpu_validation validate(std::uint64_t count, std::uint32_t k = 1000,
+                                 std::uint64_t lag = 1) {
+        wrng_gpu_validation v{};
+        detail::check(wrng_gpu_validate(g_, count, k, lag, nullptr, nullptr, &v), g_,
+                      "validate");
+        return v;
+    }
 
     std::vector<std::uint8_t> save_state() const {
         std::size_t n = 0;
