@@ -41,6 +41,10 @@ struct DeviceGuard {
 // WRNG_GPU_NO_BULK=1 routes full-refill emission through warp stores (A/B
 // measurements); the default is the bulk-copy engine.
 const bool g_bulk_emit = std::getenv("WRNG_GPU_NO_BULK") == nullptr;
+// WRNG_GPU_CLUSTER=1 runs few-pool fills on the cluster engine (opt-in: its
+// random DSMEM gathers are request-bound, slower than one CTA for C1;
+// DESIGN.md §5).
+const bool g_cluster = std::getenv("WRNG_GPU_CLUSTER") != nullptr;
 
 bool crossed(uint64_t before, uint64_t after, uint64_t period) {
     return period > 0 && after / period > before / period;  // wallace.cpp:182-184
@@ -341,7 +345,11 @@ wrng_gpu_status fill_device(wrng_gpu* g, void* out, int out_f32, const OutLayout
         a.sigma = sigma;
         a.lay = lay;
         a.bulk_emit = g_bulk_emit && (reinterpret_cast<uintptr_t>(out) % (out_f32 ? 4 : 8)) == 0;
-        LAUNCH(launch_smem(g->cfg.n_arrays, g->cfg.dtype, a, s));
+        if (g_cluster && g->cfg.restart_interval_passes == 0 &&
+            cluster_engine_fits(g->cfg.n_arrays, g->cfg.dtype, g->N, P))
+            LAUNCH(launch_cluster(g->cfg.n_arrays, g->cfg.dtype, a, s));
+        else
+            LAUNCH(launch_smem(g->cfg.n_arrays, g->cfg.dtype, a, s));
         for (uint32_t p = 0; p < P; ++p)
             plan_fill(g, g->ctr[p], lay.len_base + (p < lay.len_extra ? 1 : 0), nullptr);
         return WRNG_GPU_OK;

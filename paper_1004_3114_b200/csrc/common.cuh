@@ -442,9 +442,18 @@ __device__ __forceinline__ double sq_term(T v) {
 }
 
 // CTA-cooperative exact direct_sumsq of v[0, n) (shared or global memory).
-// Uses min(blockDim, 64) chunks; `scratch` (shared) needs 32 bytes per
-// chunk (2 KiB).  Must be called by all threads; returns the sum to all.
-constexpr uint32_t kSumScratchBytes = 64 * sizeof(SumSeg);
+// Chunks: up to min(blockDim, max_chunks) (one per thread), guessed binades
+// from a block scan of approximate chunk sums; blocks of kSumBlk chunks are
+// pre-composed in parallel, so the serial walk is O(chunks / kSumBlk) plus a
+// chunk- or term-level fallback only where a guess fails (near powers of
+// two).  `scratch` (shared) needs sum_scratch_bytes(max_chunks) bytes.
+// Must be called by all threads; returns the sum to all.
+constexpr uint32_t kSumBlk = 16;
+__host__ __device__ constexpr uint32_t sum_scratch_bytes(uint32_t max_chunks) {
+    return (uint32_t)sizeof(SumSeg) * (max_chunks + (max_chunks + kSumBlk - 1) / kSumBlk);
+}
+constexpr uint32_t kSumSmallChunks = 60;  // 60 + 4 segments: the 2 KiB word buffer
+static_assert(sum_scratch_bytes(kSumSmallChunks) <= 2048, "word buffer");
 
 // A pool whose arrays (length mask + 1) are each stored rotated by `rot`:
 // value i lives at (i & ~mask) | ((i + rot) & mask).
@@ -458,27 +467,47 @@ struct RotView {
 };
 
 template <typename T, typename V = const T*>
-__device__ double exact_sumsq_cta(V v, uint32_t n, void* scratch) {
-    const uint32_t nch = blockDim.x < 64 ? blockDim.x : 64;
-    uint32_t c = n / nch;  // odd chunk length: conflict-free shared reads
-    if (c > 1 && (c & 1) == 0) c -= 1;
+__device__ double exact_sumsq_cta(V v, uint32_t n, void* scratch,
+                                  uint32_t max_chunks = kSumSmallChunks) {
+    uint32_t nch = blockDim.x < max_chunks ? blockDim.x : max_chunks;
+    if (nch > n) nch = n > 0 ? n : 1;
+    // balanced chunks of c = ceil(n / nch) values, rounded up to odd (lane
+    // stride c: conflict-free shared reads); the last chunk takes the rest
+    uint32_t c = (n + nch - 1) / nch;
+    if (c > 1 && (c & 1) == 0) c += 1;
+    nch = (n + c - 1) / c;
+    const uint32_t nblk = (nch + kSumBlk - 1) / kSumBlk;
     SumSeg* seg = static_cast<SumSeg*>(scratch);
-    double* pref = static_cast<double*>(scratch);  // aliases seg[], used first
-    const uint32_t t = threadIdx.x;
-    const uint32_t lo = t * c, hi = t + 1 == nch ? n : (t + 1) * c;
-    // pass 1: approximate chunk sums -> exclusive prefix (binade guesses)
+    SumSeg* blk = seg + nch;
+    double* wsum = static_cast<double*>(scratch);  // warp totals, before seg[] is written
+    const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
+    const uint32_t lo = t * c, hi = t + 1 == nch ? n : (t + 1) * c;  // used for t < nch
+    // pass 1: approximate chunk sums -> exclusive block scan (binade guesses)
     double a = 0.0;
     if (t < nch)
         for (uint32_t i = lo; i < hi; ++i) a += sq_term(v[i]);
-    __syncthreads();
-    if (t < nch) pref[t] = a;
-    __syncthreads();
-    int e = -2000;
-    if (t < nch) {
-        double pre = 0.0;
-        for (uint32_t j = 0; j < t; ++j) pre += pref[j];
-        if (pre > 0.0) e = exp2_of(pre);
+    double x = a;
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
     }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t nw = (blockDim.x + 31) / 32;
+        double w = lane < nw ? wsum[lane] : 0.0;
+#pragma unroll
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        wsum[lane] = w;
+    }
+    __syncthreads();
+    const double pre = x - a + (warp > 0 ? wsum[warp - 1] : 0.0);
+    const int e = (t < nch && pre > 0.0) ? exp2_of(pre) : -2000;
+    __syncthreads();  // wsum aliases seg[]
     // pass 2: segment function of the chunk in its guessed binade
     SumSeg g;
     seg_init(g, e);
@@ -488,25 +517,35 @@ __device__ double exact_sumsq_cta(V v, uint32_t n, void* scratch) {
     } else {
         g.valid = 0;
     }
+    if (t < nch) seg[t] = g;
     __syncthreads();
-    if (t < nch) {
-        seg_finalize(g);
-        seg[t] = g;
+    // blocks of kSumBlk chunks composed in parallel (valid only within one binade)
+    if (t < nblk) {
+        SumSeg b = seg[t * kSumBlk];
+        const uint32_t kend = (t + 1) * kSumBlk < nch ? (t + 1) * kSumBlk : nch;
+        for (uint32_t k = t * kSumBlk + 1; k < kend; ++k) b = seg_compose(b, seg[k]);
+        seg_finalize(b);
+        blk[t] = b;
     }
     __syncthreads();
-    // walk (one thread): O(1) per chunk, term by term only where needed
-    double q = 0.0;
+    // walk (one thread): per block, else per chunk, else term by term
     if (t == 0) {
-        for (uint32_t k = 0; k < nch; ++k) {
-            if (seg_apply(q, seg[k])) continue;
-            const uint32_t l2 = k * c, h2 = k + 1 == nch ? n : (k + 1) * c;
-            for (uint32_t i = l2; i < h2; ++i) q = q + sq_term(v[i]);
+        double q = 0.0;
+        for (uint32_t bi = 0; bi < nblk; ++bi) {
+            if (seg_apply(q, blk[bi])) continue;
+            const uint32_t kend = (bi + 1) * kSumBlk < nch ? (bi + 1) * kSumBlk : nch;
+            for (uint32_t k = bi * kSumBlk; k < kend; ++k) {
+                SumSeg gk = seg[k];
+                seg_finalize(gk);
+                if (seg_apply(q, gk)) continue;
+                const uint32_t l2 = k * c, h2 = k + 1 == nch ? n : (k + 1) * c;
+                for (uint32_t i = l2; i < h2; ++i) q = q + sq_term(v[i]);
+            }
         }
+        *reinterpret_cast<double*>(blk) = q;
     }
     __syncthreads();
-    if (t == 0) pref[0] = q;
-    __syncthreads();
-    q = pref[0];
+    const double q = *reinterpret_cast<const double*>(blk);
     __syncthreads();
     return q;
 }
@@ -516,7 +555,8 @@ __device__ double exact_sumsq_cta(V v, uint32_t n, void* scratch) {
 // tracked = sequential sum.  Consumes n*N + 2 uniforms.
 template <typename T>
 __device__ void init_pool_dev(T* pool, uint64_t nvals, uint64_t* tab, Ctl* ctl,
-                              uint64_t* wbuf, uint32_t step) {
+                              uint64_t* wbuf, uint32_t step, void* sum_scratch = nullptr,
+                              uint32_t sum_chunks = kSumSmallChunks) {
     lfg_bulk(tab, ctl, wbuf, nvals + 2, step, [&](uint64_t base, uint32_t cnt) {
         for (uint32_t k = threadIdx.x; k < cnt / 2; k += blockDim.x) {
             double x, y;
@@ -532,12 +572,31 @@ __device__ void init_pool_dev(T* pool, uint64_t nvals, uint64_t* tab, Ctl* ctl,
         }
     });
     // tracked = direct_sumsq (exact left-to-right value, computed in parallel)
-    const double q = exact_sumsq_cta<T>(pool, (uint32_t)nvals, wbuf);
+    const double q = exact_sumsq_cta<T>(pool, (uint32_t)nvals, sum_scratch ? sum_scratch : wbuf,
+                                        sum_scratch ? sum_chunks : kSumSmallChunks);
     if (threadIdx.x == 0) {
         ctl->draws += nvals + 2;
         ctl->tracked = q;
     }
     __syncthreads();
 }
+
+// Passes-until-boundary bookkeeping without divisions in the refill loop:
+// crossed(before, before + f, P) (wallace.cpp:182-184) <=> (before mod P) + f >= P.
+struct PeriodCounter {
+    uint64_t period, rem;
+    __device__ __forceinline__ void init(uint64_t P, uint64_t pc) {
+        period = P;
+        rem = P ? pc % P : 0;
+    }
+    __device__ __forceinline__ bool will_cross(uint64_t f) const {
+        return period > 0 && rem + f >= period;
+    }
+    __device__ __forceinline__ void advance(uint64_t f) {
+        if (!period) return;
+        rem += f;
+        while (rem >= period) rem -= period;
+    }
+};
 
 }  // namespace wg

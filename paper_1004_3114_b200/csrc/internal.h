@@ -96,6 +96,12 @@ cudaError_t launch_smem(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
 // aligned pool layout needs its low bits to be 0x400).
 void smem_engine_probe(cudaStream_t st);
 
+// Cluster engine (cluster_engine.cu): one pool over a cluster of 8 CTAs,
+// fills without restarts.
+bool cluster_engine_fits(uint32_t n_arrays, uint32_t dtype, uint32_t N, uint32_t pools);
+cudaError_t launch_cluster(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
+                           cudaStream_t st);
+
 // HBM engine: one grid-wide launch per pass.
 struct HbmPass {
     uint32_t src;        // buffer index read

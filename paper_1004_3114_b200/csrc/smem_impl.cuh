@@ -81,7 +81,14 @@ struct SmemShape {
     static constexpr uint32_t POOL_OFF =
         CAN_ALIGN ? ((kDynSmemBase + HEAD + ABYTES - 1) / ABYTES) * ABYTES - kDynSmemBase
                   : HEAD;
-    static constexpr uint32_t BYTES = POOL_OFF + (uint32_t)(NVALS * sizeof(T));
+    static constexpr uint32_t POOL_END = POOL_OFF + (uint32_t)(NVALS * sizeof(T));
+    // exact-sum scratch: pools of >= 96 KiB run one CTA per SM anyway, so the
+    // drift audit gets up to 512 chunks (short serial chains); smaller pools
+    // reuse the 2 KiB word buffer (60 chunks) to keep their occupancy
+    static constexpr bool BIGSUM = NVALS * sizeof(T) >= 96 * 1024;
+    static constexpr uint32_t SUM_CHUNKS = BIGSUM ? (NTH < 512 ? NTH : 512) : kSumSmallChunks;
+    static constexpr uint32_t SCR_OFF = BIGSUM ? ((POOL_END + 15) & ~15u) : WBUF_OFF;
+    static constexpr uint32_t BYTES = BIGSUM ? SCR_OFF + sum_scratch_bytes(SUM_CHUNKS) : POOL_END;
 };
 
 template <int B, int E, typename F>
@@ -570,7 +577,8 @@ __device__ __forceinline__ bool smem_drift_check() {
     using S = SmemShape<T, NA, LOGN>;
     Ctl* ctl = &sm_at<Ctl>(S::CTL_OFF);
     const RotView<T> v{&sm_at<T>(S::POOL_OFF), S::MASK, ctl->rot};
-    const double rec = exact_sumsq_cta<T>(v, (uint32_t)S::NVALS, &sm_at<uint64_t>(S::WBUF_OFF));
+    const double rec =
+        exact_sumsq_cta<T>(v, (uint32_t)S::NVALS, &sm_at<uint64_t>(S::SCR_OFF), S::SUM_CHUNKS);
     if (threadIdx.x == 0) {
         const double rel = fabs(rec / ctl->tracked - 1.0);
         if (!(rel <= 1e-3))
@@ -586,28 +594,11 @@ template <typename T, int NA, int LOGN>
 __device__ __forceinline__ void smem_restart() {
     using S = SmemShape<T, NA, LOGN>;
     init_pool_dev(&sm_at<T>(S::POOL_OFF), S::NVALS, &sm_at<uint64_t>(S::TAB_OFF),
-                  &sm_at<Ctl>(S::CTL_OFF), &sm_at<uint64_t>(S::WBUF_OFF), S::STEP);
+                  &sm_at<Ctl>(S::CTL_OFF), &sm_at<uint64_t>(S::WBUF_OFF), S::STEP,
+                  &sm_at<uint64_t>(S::SCR_OFF), S::SUM_CHUNKS);
     if (threadIdx.x == 0) sm_at<Ctl>(S::CTL_OFF).rot = 0;  // natural order again
     __syncthreads();
 }
-
-// Passes-until-boundary bookkeeping without divisions in the refill loop:
-// crossed(before, before + f, P) (wallace.cpp:182-184) <=> (before mod P) + f >= P.
-struct PeriodCounter {
-    uint64_t period, rem;
-    __device__ __forceinline__ void init(uint64_t P, uint64_t pc) {
-        period = P;
-        rem = P ? pc % P : 0;
-    }
-    __device__ __forceinline__ bool will_cross(uint64_t f) const {
-        return period > 0 && rem + f >= period;
-    }
-    __device__ __forceinline__ void advance(uint64_t f) {
-        if (!period) return;
-        rem += f;
-        while (rem >= period) rem -= period;
-    }
-};
 
 template <typename T, int NA, int LOGN, int EM, bool AL>
 __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, LOGN>::MINB)

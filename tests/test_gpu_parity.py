@@ -349,6 +349,39 @@ def test_bulk_and_warp_store_emission_agree(W, dt, n):
     assert outs[0] == outs[1]
 
 
+@pytest.mark.parametrize("n,dt,p", [(4, "f64", 12), (2, "f64", 11), (4, "f32", 13)])
+def test_cluster_engine_matches_oracle(W, n, dt, p):
+    """The opt-in cluster engine (WRNG_GPU_CLUSTER=1, one pool over 8 CTAs,
+    DSMEM gathers) is bit-identical to the oracle through drift audits,
+    leftovers and fp32/fp64 outputs (subprocess: the switch is read at load)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, sys\n"
+        "sys.path.insert(0, 'oracle')\n"
+        "import oracle as O, torch\n"
+        "import paper_1004_3114_b200 as W\n"
+        f"kw = dict(pool_exponent={p}, throwaway_f=2, seed=31, n_arrays={n}, dtype='{dt}',"
+        " drift_check_period=3)\n"
+        "g = W.WallaceState(W.WallaceConfig(init_on_host=True, **kw))\n"
+        f"o = O.OracleState(pool_exponent={p}, throwaway_f=2, seed=31, n_arrays={n},"
+        f" dtype=O.{'F64' if dt == 'f64' else 'F32'}, drift_period=3)\n"
+        f"tdt = torch.{'float64' if dt == 'f64' else 'float32'}\n"
+        "ok = True\n"
+        f"for c in (5 * {n} * 2**{p} + 17, 3 * {n} * 2**{p} - 5, 1000):\n"
+        "    t = torch.empty(c, dtype=tdt, device='cuda'); g.fill(t); torch.cuda.synchronize()\n"
+        "    ok &= bool(np.array_equal(t.cpu().numpy(), o.fill(c)))\n"
+        "pv, pt, pw = o.pool(); gp = g.active_pool()\n"
+        "ok &= bool(np.array_equal(gp.arrays.reshape(-1), pv)) and gp.tracked_sumsq == pt\n"
+        "print('OK' if ok else 'MISMATCH')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       timeout=300, env=dict(os.environ, WRNG_GPU_CLUSTER="1"))
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.strip().splitlines()[-1] == "OK"
+
+
 def test_host_fill_larger_than_staging(W):
     """Host output larger than the 2 x 256 MiB staging slabs (f32 bank)."""
     g = gpu_state(W, pool_exponent=10, throwaway_f=1, seed=31, n_arrays=4, dtype="f32", pools=148,
