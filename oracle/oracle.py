@@ -195,6 +195,9 @@ def ref_lib():
         lib.ref_state_load.argtypes = [vp, C.c_size_t, C.POINTER(vp)]
         lib.ref_bench_threads.restype = dbl
         lib.ref_bench_threads.argtypes = [u32, u32, u8, u64, u64, u32, u64, u32]
+        lib.ref_bench_array.restype = dbl
+        lib.ref_bench_array.argtypes = [u32, u32, u8, u64, u64, u32, u64, u64,
+                                        C.c_void_p]
         _ref_lib = lib
     return _ref_lib
 
@@ -514,6 +517,15 @@ class RefState:
         buf = (C.c_uint8 * len(data)).from_buffer_copy(data)
         _check(lib.ref_state_load(buf, len(data), C.byref(h)), "load_state")
         return cls(_handle=h)
+
+
+def ref_bench_array(pool_exponent, f, mode, seed, stream0, threads, per_thread, out,
+                    chunk=1 << 16) -> float:
+    """Reference threads filling their segments of one host array `out`
+    (float64, >= threads * per_thread values); returns wall seconds."""
+    assert out.dtype == np.float64 and out.size >= threads * per_thread
+    return ref_lib().ref_bench_array(pool_exponent, f, mode, seed, stream0, threads,
+                                     per_thread, chunk, out.ctypes.data)
 
 
 def ref_bench_threads(pool_exponent, f, mode, seed, stream0, threads, per_thread,

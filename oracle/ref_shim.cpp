@@ -355,4 +355,39 @@ double ref_bench_threads(uint32_t pool_exponent, uint32_t f, uint8_t mode,
     return std::chrono::duration<double>(t1 - t0).count();
 }
 
+// ---- the same threads filling one large host array: thread t fills its
+// own contiguous segment out[t * per_thread, (t + 1) * per_thread) with one
+// fill(span) call per `chunk` values, so every normal lands in memory (the
+// shape of bench.py's workload and of its host-output e2e leg).
+double ref_bench_array(uint32_t pool_exponent, uint32_t f, uint8_t mode, uint64_t seed,
+                       uint64_t stream0, uint32_t threads, uint64_t per_thread,
+                       uint64_t chunk, double* out) {
+    std::vector<WallaceState> states;
+    states.reserve(threads);
+    for (uint32_t t = 0; t < threads; ++t) {
+        WallaceConfig cfg;
+        cfg.pool_exponent = pool_exponent;
+        cfg.throwaway_f = f;
+        cfg.scale_mode = static_cast<ScaleMode>(mode);
+        cfg.seed = seed;
+        cfg.stream_id = stream0 + t;
+        states.emplace_back(cfg);
+    }
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> ws;
+    for (uint32_t t = 0; t < threads; ++t) {
+        ws.emplace_back([&, t] {
+            double* seg = out + (uint64_t)t * per_thread;
+            for (uint64_t done = 0; done < per_thread;) {
+                const uint64_t take = per_thread - done < chunk ? per_thread - done : chunk;
+                states[t].fill(std::span<double>(seg + done, take), 0.0, 1.0);
+                done += take;
+            }
+        });
+    }
+    for (auto& w : ws) w.join();
+    auto t1 = std::chrono::steady_clock::now();
+    return std::chrono::duration<double>(t1 - t0).count();
+}
+
 }  // extern "C"

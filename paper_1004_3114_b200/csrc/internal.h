@@ -77,7 +77,8 @@ struct KernelArgs {
     uint64_t l2_bytes;
     float l2_hit;
     // smem engine: full refills leave shared memory through the bulk-copy
-    // engine (output must be aligned to its element size)
+    // engine (output must be aligned to its element size); the value is the
+    // output alignment in bytes of each bulk span (0 = warp stores only)
     uint32_t bulk_emit;
 };
 

@@ -33,8 +33,20 @@
 #ifndef WG_EXP_NOSTG
 #define WG_EXP_NOSTG 0
 #endif
+#ifndef WG_EXP_NORAGGED  // experiment only: drop the ragged-end warp stores
+#define WG_EXP_NORAGGED 0
+#endif
+#ifndef WG_EXP_NOBULK  // experiment only: drop the bulk copies
+#define WG_EXP_NOBULK 0
+#endif
 #ifndef WG_DATA_REGS
 #define WG_DATA_REGS 64  // registers holding one thread's columns of a pass
+#endif
+#ifndef WG_DATA_REGS_F32N4
+// fp32 n = 4 pools (C3/C4): 32 columns per thread, so a 4x1024 pool is one
+// warp and the per-pass scalar work (parameter draw, chi-squared scale,
+// loop control) is amortised over 128 values per thread instead of 64
+#define WG_DATA_REGS_F32N4 128
 #endif
 
 namespace wg {
@@ -45,8 +57,8 @@ extern __shared__ __align__(16) unsigned char g_sm[];
 
 enum EmitMode : int { EM_UNIT = 0, EM_GENERIC = 1 };
 
-constexpr uint32_t pick_j(uint32_t N, uint32_t regs_per_col) {
-    uint32_t j = WG_DATA_REGS / regs_per_col;
+constexpr uint32_t pick_j(uint32_t N, uint32_t regs_per_col, uint32_t data_regs) {
+    uint32_t j = data_regs / regs_per_col;
     if (j > 32) j = 32;
     while (N / j < 32 && j > 1) j /= 2;
     while (N / j > 1024) j *= 2;
@@ -60,11 +72,12 @@ constexpr uint32_t kDynSmemBase = 0x400;
 template <typename T, int NA, int LOGN>
 struct SmemShape {
     static constexpr uint32_t N = 1u << LOGN;
-    static constexpr uint32_t J = pick_j(N, NA * (uint32_t)sizeof(T) / 4);  // columns/thread
-    static constexpr uint32_t NTH = N / J;                                  // CTA size
-    // registers/thread = 65536 / (NTH * MINB): 2*WG_DATA_REGS
-    static constexpr uint32_t MINB =
-        NTH >= 32768 / WG_DATA_REGS ? 1 : (32768 / WG_DATA_REGS) / NTH;
+    static constexpr uint32_t DREGS =
+        sizeof(T) == 4 && NA == 4 ? WG_DATA_REGS_F32N4 : WG_DATA_REGS;
+    static constexpr uint32_t J = pick_j(N, NA * (uint32_t)sizeof(T) / 4, DREGS);  // columns/thread
+    static constexpr uint32_t NTH = N / J;                                         // CTA size
+    // registers/thread = 65536 / (NTH * MINB): 2*DREGS
+    static constexpr uint32_t MINB = NTH >= 32768 / DREGS ? 1 : (32768 / DREGS) / NTH;
     static constexpr uint32_t MASK = N - 1;
     static constexpr uint32_t ABYTES = N * (uint32_t)sizeof(T);  // one array
     static constexpr uint32_t MASKB = MASK * (uint32_t)sizeof(T);
@@ -338,7 +351,8 @@ __device__ __forceinline__ void phase_c2(const f2_t (&u)[4][SmemShape<float, 4, 
                 sts_rot<float, 4, LOGN, m, k>(pc, MD == 3 ? e[h] : y[h]);
                 if constexpr (MD == 3) {
                     if constexpr (k == 0 || k == (int)S::J - 1) {
-                        if (md3_own<float, 4, LOGN, m, k>(pc, tid)) ob[col] = e[h];
+                        if (!WG_EXP_NORAGGED && md3_own<float, 4, LOGN, m, k>(pc, tid))
+                            ob[col] = e[h];
                     }
                 } else if constexpr (MD == 1) {
 #if !WG_EXP_NOSTG  // experiment only: drop the output stores to bound their cost
@@ -458,8 +472,9 @@ __device__ __forceinline__ void bc_barrier(bool bulk_on) {
 template <typename T, int NA, int LOGN, int EM, bool AL, bool COLD>
 __device__ __forceinline__ bool smem_pass(uint32_t pool_s, uint32_t mode, uint32_t emit_n,
                                           char* out_p, const EmitCfg& ec, wrng_gpu_params* rec,
-                                          bool prefetch, T* prev, int slot, bool bulk_on) {
+                                          bool prefetch, T* prev, int slot, uint32_t bvec) {
     using S = SmemShape<T, NA, LOGN>;
+    const bool bulk_on = bvec != 0;
     constexpr uint32_t N = S::N, NTH = S::NTH;
     const uint32_t tid = threadIdx.x;
     Ctl* ctl = &sm_at<Ctl>(S::CTL_OFF);
@@ -528,9 +543,15 @@ __device__ __forceinline__ bool smem_pass(uint32_t pool_s, uint32_t mode, uint32
         const uint32_t lastb = (((uint32_t)(S::J - 1) * NTH + tid + rot2) * ES) & S::MASKB;
         pc.last_s = AL ? (lastb | pool_s) : (lastb + pool_s);
     }
-    pc.j0 = (VEC - rot2) & (VEC - 1);
-    pc.jend = pc.j0 + ((N - rot2 - pc.j0) & ~(VEC - 1));
-    pc.jend_last = pc.j0 + ((umin32(N - rot2, N - 1) - pc.j0) & ~(VEC - 1));
+    // bulk-copied span [j0, jend): starts and ends on a bvec-element boundary
+    // of the output (bvec >= VEC, a power of 2; 128 B lines by default)
+    {
+        const uint32_t bv = bulk_on ? bvec : VEC;
+        const uint32_t ph = (uint32_t)(reinterpret_cast<uintptr_t>(out_p) / ES) & (bv - 1);
+        pc.j0 = (bv - ph) & (bv - 1);
+        pc.jend = pc.j0 + ((N - rot2 - pc.j0) & ~(bv - 1));
+        pc.jend_last = pc.j0 + ((umin32(N - rot2, N - 1) - pc.j0) & ~(bv - 1));
+    }
     if constexpr (sizeof(T) == 4 && NA == 4 && S::J % 2 == 0) {
         f2_t u[4][S::J / 2];
         if (variant == 0)
@@ -561,7 +582,7 @@ __device__ __forceinline__ bool smem_pass(uint32_t pool_s, uint32_t mode, uint32
 #pragma unroll
         for (int m = 0; m < NA; ++m) {
             const uint32_t je = m == NA - 1 ? pc.jend_last : pc.jend;
-            if (je > pc.j0)
+            if (je > pc.j0 && !WG_EXP_NOBULK)
                 bulk_store(ob + ((uint64_t)m * N + pc.j0) * ES,
                            pool_s + (uint32_t)m * S::ABYTES + (pc.j0 + rot2) * ES,
                            (je - pc.j0) * ES);
@@ -666,6 +687,15 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
     const uint32_t mode = a.mode;
     const EmitCfg ec{a.mu, a.sigma, a.out_f32, a.unit};
     const bool bulk_on = EM == EM_UNIT && op == OP_FILL && a.bulk_emit != 0;
+    // bulk span alignment in elements: the ragged head (< bvec) and tail
+    // (< bvec + VEC) must stay inside column groups 0 and J - 1
+    constexpr uint32_t kVec = 16 / (uint32_t)sizeof(T);
+    uint32_t bvec = 0;
+    if (bulk_on) {
+        bvec = kVec;
+        const uint32_t want = a.bulk_emit / (uint32_t)sizeof(T);
+        while (bvec * 2 <= want && bvec * 2 + kVec <= NTH + 2) bvec *= 2;
+    }
     PeriodCounter drift, restart;
     drift.init(a.drift, pc);
     restart.init(a.restart, pc);
@@ -740,9 +770,9 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
             const bool ok =
                 last_launch
                     ? smem_pass<T, NA, LOGN, EM, AL, true>(pool_s, mode, en, out_p, ec, nullptr,
-                                                           prefetch, prev_buf(), slot, bulk_on)
+                                                           prefetch, prev_buf(), slot, bvec)
                     : smem_pass<T, NA, LOGN, EM, AL, false>(pool_s, mode, en, out_p, ec, nullptr,
-                                                            prefetch, nullptr, slot, bulk_on);
+                                                            prefetch, nullptr, slot, bvec);
             if (!ok) {
                 err = ctl->error;
                 break;
@@ -782,7 +812,7 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
             if (!smem_pass<T, NA, LOGN, EM, AL, true>(pool_s, mode, 0u, nullptr, ec, rec,
                                                       !last_launch,
                                                       last_launch ? prev_buf() : nullptr, slot,
-                                                      false)) {
+                                                      0u)) {
                 err = ctl->error;
                 break;
             }

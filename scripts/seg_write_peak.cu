@@ -13,6 +13,10 @@
 //   mode 7: as 1 but CTA p starts at chunk (37 p) mod nchunks (decorrelated)
 //   mode 8+: bulk, aligned chunks of CB bytes, P2 CTAs, queue Q, optional
 //            L2 evict_first hint (see table in main)
+//   mode 16+: C3's exact segments and refill boundaries (4095 values), but
+//            each refill's copy is [first U-aligned byte of the not yet
+//            written part, last U-aligned byte of the refill): what a
+//            CTA-side carry buffer of U bytes would emit (U = 128 .. 16384)
 // nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a scripts/seg_write_peak.cu -o scripts/seg_write_peak.bin
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -126,6 +130,32 @@ __global__ void __launch_bounds__(32) k_bulk_gen(char* out, uint64_t seg, uint32
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+__global__ void __launch_bounds__(64) k_bulk_carry(float* out, uint64_t seg, uint32_t ub) {
+    extern __shared__ __align__(1024) float sm[];
+    for (int i = threadIdx.x; i < (ub <= 4096 ? 6144 : 9216); i += 64) sm[i] = (float)blockIdx.x;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    float* o = out + (uint64_t)blockIdx.x * seg;
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(sm);
+    const uint64_t end = reinterpret_cast<uint64_t>(o + seg);
+    uint64_t from = reinterpret_cast<uint64_t>(o) & ~15ull;  // written up to here
+    for (uint64_t done = 0; done < seg; done += kChunk) {
+        const uint64_t n = seg - done < kChunk ? seg - done : kChunk;
+        uint64_t e = reinterpret_cast<uint64_t>(o + done + n);
+        e = e >= end ? (e & ~15ull) : (e & ~(uint64_t)(ub - 1));
+        if (e > from) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(from),
+                         "r"(s), "r"((uint32_t)(e - from))
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            from = e;
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __global__ void k_fill8(float* out, uint64_t n8) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n8;
          i += (uint64_t)gridDim.x * blockDim.x)
@@ -175,7 +205,27 @@ int main(int argc, char** argv) {
     // mode 8..: {chunk bytes, CTAs per SM, queue, hint}
     const int gen[][4] = {{16384, 8, 4, 0}, {4096, 8, 4, 0}, {65536, 2, 4, 0}, {16384, 8, 4, 1},
                           {16384, 4, 4, 0}, {16384, 14, 4, 0}, {32768, 6, 4, 0}, {16384, 8, 1, 0}};
-    for (int mode = 0; mode < 16; ++mode) {
+    cudaFuncSetAttribute(k_bulk_carry, cudaFuncAttributeMaxDynamicSharedMemorySize, 36864);
+    const int nmodes = argc > 2 ? atoi(argv[2]) : 16;
+    const uint32_t carry_u[] = {16, 128, 512, 1024, 2048, 4096, 16384};
+    for (int mode = 0; mode < nmodes; ++mode) {
+        if (mode >= 16) {
+            const uint32_t ub = carry_u[(mode - 16) % 7];
+            float best = 1e30f;
+            for (int rep = 0; rep < 5; ++rep) {
+                cudaEventRecord(a);
+                k_bulk_carry<<<P, 64, ub <= 4096 ? 24576 : 36864>>>(out, seg, ub);
+                cudaEventRecord(b);
+                cudaEventSynchronize(b);
+                float ms = 0;
+                cudaEventElapsedTime(&ms, a, b);
+                if (rep > 0 && ms < best) best = ms;
+            }
+            cudaError_t e = cudaGetLastError();
+            printf("{\"mode\": %d, \"carry_bytes\": %u, \"ms\": %.3f, \"gbs\": %.1f, \"err\": \"%s\"}\n",
+                   mode, ub, best, (double)(P * seg) * 4 / (best / 1e3) / 1e9, cudaGetErrorString(e));
+            continue;
+        }
         if (mode >= 8) {
             const int* gcfg = gen[mode - 8];
             const int P2 = 148 * gcfg[1];
