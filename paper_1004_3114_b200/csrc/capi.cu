@@ -41,6 +41,14 @@ struct DeviceGuard {
 // WRNG_GPU_NO_BULK=1 routes full-refill emission through warp stores (A/B
 // measurements); the default is the bulk-copy engine.
 const bool g_bulk_emit = std::getenv("WRNG_GPU_NO_BULK") == nullptr;
+// Output alignment (bytes) of each bulk-copied span; the ragged ends leave
+// through warp stores.  WRNG_GPU_BULK_ALIGN overrides it (A/B measurements).
+uint32_t bulk_align_bytes() {
+    const char* e = std::getenv("WRNG_GPU_BULK_ALIGN");
+    const long v = e ? std::strtol(e, nullptr, 10) : 64;
+    return v >= 16 && v <= 4096 && (v & (v - 1)) == 0 ? (uint32_t)v : 64u;
+}
+const uint32_t g_bulk_align = bulk_align_bytes();
 // WRNG_GPU_CLUSTER=1 runs few-pool fills on the cluster engine (opt-in: its
 // random DSMEM gathers are request-bound, slower than one CTA for C1;
 // DESIGN.md §5).
@@ -344,7 +352,9 @@ wrng_gpu_status fill_device(wrng_gpu* g, void* out, int out_f32, const OutLayout
         a.mu = mu;
         a.sigma = sigma;
         a.lay = lay;
-        a.bulk_emit = g_bulk_emit && (reinterpret_cast<uintptr_t>(out) % (out_f32 ? 4 : 8)) == 0;
+        a.bulk_emit = g_bulk_emit && (reinterpret_cast<uintptr_t>(out) % (out_f32 ? 4 : 8)) == 0
+                          ? g_bulk_align
+                          : 0u;
         if (g_cluster && g->cfg.restart_interval_passes == 0 &&
             cluster_engine_fits(g->cfg.n_arrays, g->cfg.dtype, g->N, P))
             LAUNCH(launch_cluster(g->cfg.n_arrays, g->cfg.dtype, a, s));

@@ -173,6 +173,10 @@ __device__ __forceinline__ void bulk_commit() {
 __device__ __forceinline__ void bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read_n() {  // <= N groups still reading
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void bulk_wait_all() {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -188,7 +192,19 @@ __device__ __forceinline__ void fence_async_smem() {
 struct PhaseC {
     uint32_t my_s, last_s;
     uint32_t j0, jend, jend_last;
+    uint32_t src0;  // shared address of array 0's bulk span (value j0)
 };
+
+// Experiment (off): one-warp fp32 n = 4 pools issue their bulk copies array
+// by array from phase C (phase_c2_split) instead of once per pass.  Measured
+// slower on C3 (11.95-11.99 ms vs 11.62-11.70 ms per step).
+#ifndef WG_EXP_SPLIT
+#define WG_EXP_SPLIT 0
+#endif
+template <typename T, int NA, int LOGN>
+constexpr bool kSplitC = WG_EXP_SPLIT && sizeof(T) == 4 && NA == 4 &&
+                         SmemShape<T, NA, LOGN>::NTH == 32 &&
+                         SmemShape<T, NA, LOGN>::J % 2 == 0;
 
 // Phase B: gather + unscaled transform (VAR = n=4 matrix variant; AL =
 // aligned pool base, gather address = (idx & mask) | base).
@@ -312,7 +328,7 @@ __device__ __forceinline__ bool md3_own(const PhaseC& pc, uint32_t tid) {
     using S = SmemShape<T, NA, LOGN>;
     bool own = false;
     if constexpr (K == 0) own = tid < pc.j0;
-    if constexpr (K == (int)S::J - 1) {
+    if constexpr (K + 2 >= (int)S::J) {  // the ragged tail spans <= 2 column groups
         const uint32_t j = (uint32_t)K * S::NTH + tid;
         if constexpr (M == NA - 1)
             own = own || (j >= pc.jend_last && j != S::N - 1);
@@ -327,6 +343,58 @@ __device__ __forceinline__ bool md3_own(const PhaseC& pc, uint32_t tid) {
 // 2: partial window / generic output; 3: full refill through the bulk-copy
 // engine (the pool holds the emitted form 0 + v, which differs from v only
 // for v = -0.0; the warps store only the ragged ends).
+// MD 3 on a one-warp pool (NTH == 32): array-major, so each array's bulk
+// copy leaves as soon as the array is written (lane 0 issues it after a
+// __syncwarp), and before rewriting array m lane 0 waits only for the
+// previous refill's copy of array m (bulk groups retire in order).
+template <int LOGN>
+__device__ __forceinline__ void phase_c2_split(
+    const f2_t (&u)[4][SmemShape<float, 4, LOGN>::J / 2], float c0, const PhaseC& pc,
+    char* out_p, double& withheld_out) {
+    using S = SmemShape<float, 4, LOGN>;
+    static_assert(S::NTH == 32, "one-warp pools");
+    const uint32_t tid = threadIdx.x;
+    float* ob = reinterpret_cast<float*>(out_p) + tid;
+    const f2_t C = f2_pack(c0, c0), Z = f2_pack(0.0f, 0.0f);
+    sfor<0, 4>([&](auto mc) {
+        constexpr int m = decltype(mc)::value;
+        if (tid == 0) bulk_wait_read_n<3 - m>();
+        __syncwarp();
+        sfor<0, (int)S::J / 2>([&](auto kc) {
+            constexpr int kp = decltype(kc)::value;
+            const f2_t Y = f2_mul(C, u[m][kp]);
+            float e[2];
+            f2_unpack(f2_add(Y, Z), e[0], e[1]);  // 0 + 1 * v
+            sfor<0, 2>([&](auto hc) {
+                constexpr int h = decltype(hc)::value;
+                constexpr int k = 2 * kp + h;
+                constexpr uint32_t col = m * S::N + k * S::NTH;
+                sts_rot<float, 4, LOGN, m, k>(pc, e[h]);
+                if constexpr (k == 0 || k + 2 >= (int)S::J) {
+                    if (!WG_EXP_NORAGGED && md3_own<float, 4, LOGN, m, k>(pc, tid))
+                        ob[col] = e[h];
+                }
+                if constexpr (m == 3 && k == (int)S::J - 1) {
+                    if (tid == S::NTH - 1) {
+                        float y[2];
+                        f2_unpack(Y, y[0], y[1]);
+                        withheld_out = (double)y[h];
+                    }
+                }
+            });
+        });
+        fence_async_smem();
+        __syncwarp();
+        if (tid == 0) {
+            const uint32_t je = m == 3 ? pc.jend_last : pc.jend;
+            if (je > pc.j0 && !WG_EXP_NOBULK)
+                bulk_store(reinterpret_cast<uint64_t>(out_p) + ((uint64_t)m * S::N + pc.j0) * 4,
+                           pc.src0 + (uint32_t)m * S::ABYTES, (je - pc.j0) * 4);
+            bulk_commit();
+        }
+    });
+}
+
 template <int LOGN, int EM, int MD>
 __device__ __forceinline__ void phase_c2(const f2_t (&u)[4][SmemShape<float, 4, LOGN>::J / 2],
                                          float c0, const PhaseC& pc, char* out_p, uint32_t en,
@@ -350,7 +418,7 @@ __device__ __forceinline__ void phase_c2(const f2_t (&u)[4][SmemShape<float, 4, 
                 constexpr uint32_t col = m * S::N + k * S::NTH;
                 sts_rot<float, 4, LOGN, m, k>(pc, MD == 3 ? e[h] : y[h]);
                 if constexpr (MD == 3) {
-                    if constexpr (k == 0 || k == (int)S::J - 1) {
+                    if constexpr (k == 0 || k + 2 >= (int)S::J) {
                         if (!WG_EXP_NORAGGED && md3_own<float, 4, LOGN, m, k>(pc, tid))
                             ob[col] = e[h];
                     }
@@ -398,7 +466,7 @@ __device__ __forceinline__ void phase_c(const T (&u)[NA][SmemShape<T, NA, LOGN>:
             if constexpr (MD == 3) {
                 const T e = y[m] + (T)0;  // 0 + 1 * v: the pool is the bulk source
                 sts_rot<T, NA, LOGN, m, k>(pc, e);
-                if constexpr (k == 0 || k == (int)S::J - 1) {
+                if constexpr (k == 0 || k + 2 >= (int)S::J) {
                     if (md3_own<T, NA, LOGN, m, k>(pc, tid)) ob[col] = e;
                 }
             } else {
@@ -425,8 +493,12 @@ __device__ __forceinline__ void phase_c2_any(uint32_t md,
                                              const EmitCfg& ec, double& wh) {
     if (md == 0)
         phase_c2<LOGN, EM, 0>(u, c0, pc, out_p, 0, ec, wh);
-    else if (EM == EM_UNIT && md == 3)
-        phase_c2<LOGN, EM, 3>(u, c0, pc, out_p, en, ec, wh);
+    else if (EM == EM_UNIT && md == 3) {
+        if constexpr (kSplitC<float, 4, LOGN>)
+            phase_c2_split<LOGN>(u, c0, pc, out_p, wh);
+        else
+            phase_c2<LOGN, EM, 3>(u, c0, pc, out_p, en, ec, wh);
+    }
     else if (EM == EM_UNIT && md == 1)
         phase_c2<LOGN, EM, 1>(u, c0, pc, out_p, en, ec, wh);
     else
@@ -552,13 +624,14 @@ __device__ __forceinline__ bool smem_pass(uint32_t pool_s, uint32_t mode, uint32
         pc.jend = pc.j0 + ((N - rot2 - pc.j0) & ~(bv - 1));
         pc.jend_last = pc.j0 + ((umin32(N - rot2, N - 1) - pc.j0) & ~(bv - 1));
     }
+    pc.src0 = pool_s + (pc.j0 + rot2) * ES;
     if constexpr (sizeof(T) == 4 && NA == 4 && S::J % 2 == 0) {
         f2_t u[4][S::J / 2];
         if (variant == 0)
             phase_b2<LOGN, 0, AL>(pool_s, ixb, stepb, u);
         else
             phase_b2<LOGN, 1, AL>(pool_s, ixb, stepb, u);
-        bc_barrier<EM>(bulk_on);
+        bc_barrier<EM>(bulk_on && !(kSplitC<T, NA, LOGN> && md == 3));
         phase_c2_any<LOGN, EM>(md, u, c0, pc, out_p, emit_n, ec, wh);
     } else {
         T u[NA][S::J];
@@ -576,15 +649,14 @@ __device__ __forceinline__ bool smem_pass(uint32_t pool_s, uint32_t mode, uint32
         ctl->rot = rot2;
     }
     __syncthreads();
-    if (md == 3 && tid == 0) {
+    if (md == 3 && !kSplitC<T, NA, LOGN> && tid == 0) {
         // [j0, jend) of every array (last: jend_last) -> output, 16-byte aligned
         const uint64_t ob = reinterpret_cast<uint64_t>(out_p);
 #pragma unroll
         for (int m = 0; m < NA; ++m) {
             const uint32_t je = m == NA - 1 ? pc.jend_last : pc.jend;
             if (je > pc.j0 && !WG_EXP_NOBULK)
-                bulk_store(ob + ((uint64_t)m * N + pc.j0) * ES,
-                           pool_s + (uint32_t)m * S::ABYTES + (pc.j0 + rot2) * ES,
+                bulk_store(ob + ((uint64_t)m * N + pc.j0) * ES, pc.src0 + (uint32_t)m * S::ABYTES,
                            (je - pc.j0) * ES);
         }
         bulk_commit();
@@ -687,14 +759,15 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
     const uint32_t mode = a.mode;
     const EmitCfg ec{a.mu, a.sigma, a.out_f32, a.unit};
     const bool bulk_on = EM == EM_UNIT && op == OP_FILL && a.bulk_emit != 0;
-    // bulk span alignment in elements: the ragged head (< bvec) and tail
-    // (< bvec + VEC) must stay inside column groups 0 and J - 1
+    // bulk span alignment in elements: the ragged head (< bvec) must stay
+    // inside column group 0 and the tail (< bvec + VEC) inside the last two
     constexpr uint32_t kVec = 16 / (uint32_t)sizeof(T);
+    constexpr uint32_t kTailCols = S::J >= 2 ? 2 * NTH : NTH;
     uint32_t bvec = 0;
     if (bulk_on) {
         bvec = kVec;
         const uint32_t want = a.bulk_emit / (uint32_t)sizeof(T);
-        while (bvec * 2 <= want && bvec * 2 + kVec <= NTH + 2) bvec *= 2;
+        while (bvec * 2 <= want && bvec * 2 <= NTH && bvec * 2 + kVec <= kTailCols + 2) bvec *= 2;
     }
     PeriodCounter drift, restart;
     drift.init(a.drift, pc);
