@@ -53,6 +53,9 @@ const uint32_t g_bulk_align = bulk_align_bytes();
 // random DSMEM gathers are request-bound, slower than one CTA for C1;
 // DESIGN.md §5).
 const bool g_cluster = std::getenv("WRNG_GPU_CLUSTER") != nullptr;
+// HBM engine: consecutive passes run as one persistent launch (k_hbm_run);
+// WRNG_GPU_HBM_STEPWISE=1 launches one kernel per pass and per emission.
+const bool g_hbm_run = std::getenv("WRNG_GPU_HBM_STEPWISE") == nullptr;
 
 bool crossed(uint64_t before, uint64_t after, uint64_t period) {
     return period > 0 && after / period > before / period;  // wallace.cpp:182-184
@@ -72,6 +75,7 @@ struct wrng_gpu {
     wrng_gpu_params* params = nullptr;  // device: per-pool param records / hbm batches
     size_t params_cap = 0;
     double* scratch = nullptr;
+    unsigned long long* gbar = nullptr;  // HBM engine: k_hbm_run's grid barrier counter
     cudaStream_t stream = nullptr;       // internal stream
     cudaStream_t copy_stream = nullptr;  // D2H of staged host fills
     cudaStream_t last = nullptr;         // last stream work was queued on
@@ -307,6 +311,25 @@ wrng_gpu_status run_hbm(wrng_gpu* g, uint32_t p, Ctr c, const std::vector<Ev>& e
         uint32_t pi = 0;
         for (size_t k = i; k < jend; ++k) {
             const Ev& e = ev[k];
+            if (e.kind == Ev::PASS && g_hbm_run) {
+                // a run of consecutive passes: one persistent launch
+                HbmRun run{};
+                run.src0 = c.active;
+                run.param0 = pi;
+                while (k < jend && ev[k].kind == Ev::PASS && run.npass < kRunMax) {
+                    const Ev& q = ev[k];
+                    run.emit_n[run.npass] = q.emit_n;
+                    run.out_off[run.npass] = q.out_off;
+                    if (q.end_refill) run.end_mask |= 1ull << run.npass;
+                    ++run.npass;
+                    ++pi;
+                    c.active ^= 1u;
+                    ++k;
+                }
+                --k;
+                LAUNCH(launch_hbm_run(NA, dt, a, g->params, run, g->gbar, s));
+                continue;
+            }
             if (e.kind == Ev::EMIT) {
                 LAUNCH(launch_hbm_emit(NA, dt, a, c.active, e.pos, e.take, e.out_off, s));
             } else if (e.kind == Ev::PASS) {
@@ -705,6 +728,9 @@ wrng_gpu_status alloc_handle(const wrng_gpu_config* cfg, wrng_gpu** out) {
     CK(cudaMemset(g->meta, 0, sizeof(PoolMeta) * cfg->pools));
     CK(cudaMalloc(&g->lfg, sizeof(LfgState) * cfg->pools));
     CK(cudaMalloc(&g->scratch, g->hbm ? hbm_drift_scratch_bytes(g->nvals) : sizeof(double) * 1024));
+    if (g->hbm) {
+        CK(cudaMalloc(&g->gbar, sizeof(unsigned long long)));
+    }
     CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&g->order_ev, cudaEventDisableTiming));
@@ -854,6 +880,7 @@ void wrng_gpu_destroy(wrng_gpu_t* g) {
             if (g->lfg) cudaFree(g->lfg);
             if (g->params) cudaFree(g->params);
             if (g->scratch) cudaFree(g->scratch);
+            if (g->gbar) cudaFree(g->gbar);
             if (g->order_ev) cudaEventDestroy(g->order_ev);
             if (g->stream) cudaStreamDestroy(g->stream);
             if (g->copy_stream) cudaStreamDestroy(g->copy_stream);

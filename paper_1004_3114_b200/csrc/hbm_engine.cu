@@ -80,7 +80,13 @@ cudaError_t launch_hbm_params(uint32_t n_arrays, uint32_t N, LfgState* lfg,
 // ---------------------------------------------------------------------------
 // one regeneration pass (wallace.cpp:113-137) on transposed storage
 // ---------------------------------------------------------------------------
-constexpr uint32_t kJlo = 4;  // output rows per CTA
+#ifndef WG_HBM_JLO
+#define WG_HBM_JLO 4
+#endif
+#ifndef WG_EMIT_TS
+#define WG_EMIT_TS 64
+#endif
+constexpr uint32_t kJlo = WG_HBM_JLO;  // output rows per CTA
 
 // Output element with an evict-first (streaming) store, so the write-once
 // output stream does not push the pool buffers out of L2.
@@ -267,7 +273,7 @@ cudaError_t launch_hbm_pass(uint32_t n_arrays, uint32_t dtype, const KernelArgs&
 template <typename T>
 __global__ void __launch_bounds__(256) k_hbm_emit_t(KernelArgs a, uint32_t buf,
                                                     uint64_t emit_n, uint64_t out_off) {
-    constexpr uint32_t TS = 64;  // 64 x 64 tile, 16 loads + 16 stores per thread
+    constexpr uint32_t TS = WG_EMIT_TS;  // TS x TS tile, TS^2/256 loads + stores per thread
     __shared__ T tile[TS][TS + 1];
     if (a.meta->error) return;
     const uint32_t N = a.N;
@@ -280,8 +286,9 @@ __global__ void __launch_bounds__(256) k_hbm_emit_t(KernelArgs a, uint32_t buf,
     for (uint32_t k = 0; k < TS; k += 8) {
         const uint32_t jl = jl0 + ty + k;  // stored row
         if (jl < C) {
-            tile[ty + k][tx] = pool[(uint64_t)jl * R + jh0 + tx];
-            tile[ty + k][tx + 32] = pool[(uint64_t)jl * R + jh0 + tx + 32];
+#pragma unroll
+            for (uint32_t h = 0; h < TS; h += 32)
+                tile[ty + k][tx + h] = pool[(uint64_t)jl * R + jh0 + tx + h];
         }
     }
     __syncthreads();
@@ -304,7 +311,7 @@ cudaError_t launch_hbm_emit_t(uint32_t n_arrays, uint32_t dtype, const KernelArg
                               uint32_t buf, uint64_t emit_n, uint64_t out_off, cudaStream_t st) {
     const HbmSplit sp = hbm_split(a.N);
     const uint32_t R = 1u << sp.lr, C = 1u << sp.lc;
-    const dim3 grid(R / 64, (C + 63) / 64, n_arrays), block(32, 8);
+    const dim3 grid(R / WG_EMIT_TS, (C + WG_EMIT_TS - 1) / WG_EMIT_TS, n_arrays), block(32, 8);
     if (dtype == WRNG_GPU_F64)
         return launch_l2(k_hbm_emit_t<double>, grid, block, 0, st, a, a, buf, emit_n, out_off);
     return launch_l2(k_hbm_emit_t<float>, grid, block, 0, st, a, a, buf, emit_n, out_off);
@@ -702,4 +709,318 @@ cudaError_t launch_hbm_setmeta(PoolMeta* meta, uint64_t pass_count, uint64_t ava
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Persistent run of passes (C2): one launch executes up to kRunMax passes of
+// one pool with a grid-wide barrier between passes, instead of one pass
+// launch (+ one emission launch) each.  Every CTA stays resident (grid =
+// SMs x occupancy, cooperative launch), walks the stored rows
+// jlo = blockIdx.x, + gridDim.x, ... of each pass exactly as k_hbm_pass does
+// for its kJlo rows, and after an emitting pass streams 64 x 64 transpose
+// tiles of the new pool to the output (as k_hbm_emit_t).  Emission and the
+// next pass only READ the new pool, so they share one barrier interval; the
+// pass after that (which overwrites the emitted buffer) is behind the next
+// barrier.  Same arithmetic, same op order, bit-identical to the per-pass
+// kernels (wallace.cpp:113-137, 206-213).
+// ---------------------------------------------------------------------------
+
+// Grid barrier on a monotone arrival counter (zeroed before each launch):
+// barrier e (1, 2, ...) completes when the counter reaches e * gridDim.x.
+// Arrival is a fire-and-forget release reduction; no reset round trip.
+__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long& epoch) {
+    __syncthreads();
+    epoch += gridDim.x;
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(bar), "l"(1ull)
+                     : "memory");
+        // relaxed polling (an acquire load invalidates L1 on every poll),
+        // then one acquire fence
+        unsigned long long v;
+        do {
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
+        } while (v < epoch);
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    __syncthreads();
+}
+
+constexpr uint32_t kRunThreads = 512;
+constexpr uint32_t kRunTile = 64;
+constexpr uint32_t kRunStages = 3;  // source-row buffers in flight per CTA
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared bulk copy completing on an mbarrier (TMA, 1-D)
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+template <typename T, int NA>
+__global__ void __launch_bounds__(kRunThreads, 2)
+    k_hbm_run(KernelArgs a, wrng_gpu_params* params, HbmRun run, unsigned long long* gbar) {
+    extern __shared__ __align__(128) unsigned char hsm[];
+    const uint32_t N = a.N;
+    const HbmSplit sp = hbm_split(N);
+    const uint32_t R = 1u << sp.lr, C = 1u << sp.lc;
+    T* stage = reinterpret_cast<T*>(hsm);                          // [S][NA][R]
+    T(*tile)[kRunTile + 1] = reinterpret_cast<T(*)[kRunTile + 1]>(  // [64][65]
+        hsm + (size_t)kRunStages * NA * R * sizeof(T));
+    __shared__ __align__(8) uint64_t full[kRunStages];
+    __shared__ double s_c0, s_c1, s_target, s_scale;
+    __shared__ int s_err;
+    PoolMeta* meta = a.meta;
+    const uint32_t t = threadIdx.x;
+    const bool active_t = t < R;  // R < 512 only for forced-HBM small pools
+    const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
+    const uint32_t full_s = (uint32_t)__cvta_generic_to_shared(full);
+    const uint32_t row_bytes = R * (uint32_t)sizeof(T);
+    if (t == 0) {
+        for (uint32_t k = 0; k < kRunStages; ++k) mbar_init(full_s + 8 * k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t q = 0;  // source rows consumed by this CTA so far (stage q % S)
+    unsigned long long epoch = 0;  // grid barrier target
+
+    for (uint32_t i = 0; i < run.npass; ++i) {
+        const uint32_t src = run.src0 ^ (i & 1u), dst = src ^ 1u;
+        const wrng_gpu_params prm = params[run.param0 + i];
+        const T* spool = static_cast<const T*>(a.buf[src]);
+        T* dpool = static_cast<T*>(a.buf[dst]);
+        const uint32_t nrows = blockIdx.x < C ? (C - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+        const uint32_t q0 = q;
+        // thread 0: the sources of this CTA's k-th row of the pass -> stage (q0 + k) % S
+        auto issue = [&](uint32_t k) {
+            const uint32_t jlo = blockIdx.x + k * gridDim.x;
+            const uint32_t sb = (q0 + k) % kRunStages;
+            const uint32_t bar = full_s + 8 * sb;
+            mbar_expect_tx(bar, NA * row_bytes);
+#pragma unroll
+            for (int m = 0; m < NA; ++m) {
+                const uint32_t srow = (prm.stride[m] * jlo + prm.offset[m]) & (C - 1);
+                bulk_g2s(stage_s + (sb * NA + m) * row_bytes,
+                         spool + (uint64_t)m * N + (uint64_t)srow * R, row_bytes, bar);
+            }
+        };
+        if (t == 0) {
+            // the previous pass's pool was written by other CTAs' generic
+            // stores (ordered by the grid barrier); the async proxy reads it
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            for (uint32_t k = 0; k < nrows && k < kRunStages; ++k) issue(k);
+            int err = meta->error ? -1 : 0;
+            const double tracked = meta->tracked[src], withheld = meta->withheld[src];
+            if (!err) {
+                double scale, target;
+                err = pass_scale(tracked, withheld, NA * N, a.mode, scale, target);
+                if (!err) {
+                    s_target = target;
+                    s_scale = scale;
+                    // regenerate folds the scale into the matrix (wallace.cpp:116-117)
+                    s_c0 = NA == 2 ? prm.c * scale : (prm.variant ? scale : 0.5 * scale);
+                    s_c1 = NA == 2 ? prm.s * scale : scale;
+                }
+            }
+            s_err = err;
+        }
+        __syncthreads();
+        if (s_err) {  // every CTA reads the same state: all leave here together
+            // (rows already in flight complete into shared memory we abandon)
+            if (t == 0)
+                for (uint32_t k = 0; k < nrows && k < kRunStages; ++k)
+                    mbar_wait(full_s + 8 * ((q + k) % kRunStages), ((q + k) / kRunStages) & 1u);
+            if (s_err > 0 && blockIdx.x == 0 && t == 0) meta->error = s_err;
+            return;
+        }
+        const T c0 = (T)s_c0, c1 = (T)s_c1;  // fp32 pools: rounded once
+        const uint32_t variant = prm.variant;
+        for (uint32_t k = 0; k < nrows; ++k, ++q) {
+            const uint32_t jlo = blockIdx.x + k * gridDim.x;
+            const uint32_t sb = q % kRunStages;
+            mbar_wait(full_s + 8 * sb, (q / kRunStages) & 1u);
+            if (active_t) {
+                const T* rows = stage + (size_t)sb * NA * R;
+                T g[NA];
+#pragma unroll
+                for (int m = 0; m < NA; ++m) {
+                    const uint32_t sh = ((prm.stride[m] * jlo + prm.offset[m]) >> sp.lc) & (R - 1);
+                    g[m] = rows[m * R + ((prm.stride[m] * t + sh) & (R - 1))];
+                }
+                T y[NA];
+                if (NA == 2) {
+                    y[0] = c0 * g[0] + c1 * g[NA > 1 ? 1 : 0];
+                    y[NA > 1 ? 1 : 0] = c0 * g[NA > 1 ? 1 : 0] - c1 * g[0];
+                } else {
+                    const T a0 = g[0], a1 = g[NA > 1 ? 1 : 0], a2 = g[NA > 2 ? 2 : 0],
+                            a3 = g[NA > 3 ? 3 : 0];
+                    if (variant == 0) {
+                        const T pp = a0 + a1, qq = a0 - a1, rr = a2 + a3, s = a2 - a3;
+                        y[0] = c0 * (pp + rr);
+                        y[NA > 1 ? 1 : 0] = c0 * (qq + s);
+                        y[NA > 2 ? 2 : 0] = c0 * (pp - rr);
+                        y[NA > 3 ? 3 : 0] = c0 * (qq - s);
+                    } else {
+                        const T tt = (T)0.5 * ((a0 + a1) + (a2 + a3));
+                        y[0] = c0 * (tt - a0);
+                        y[NA > 1 ? 1 : 0] = c0 * (tt - a1);
+                        y[NA > 2 ? 2 : 0] = c0 * (tt - a2);
+                        y[NA > 3 ? 3 : 0] = c0 * (tt - a3);
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < NA; ++m) dpool[(uint64_t)m * N + (uint64_t)jlo * R + t] = y[m];
+                if (jlo == C - 1 && t == R - 1) meta->withheld[dst] = (double)y[NA - 1];
+            }
+            __syncthreads();  // stage sb fully read
+            if (t == 0 && k + kRunStages < nrows) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(k + kRunStages);
+            }
+        }
+        const bool end = (run.end_mask >> i) & 1u;
+        const uint64_t emit_n = run.emit_n[i];
+        if (blockIdx.x == 0 && t == 0) {
+            params[run.param0 + i].scale = s_scale;
+            params[run.param0 + i].target_sumsq = s_target;
+            meta->tracked[dst] = s_target;
+            meta->active = dst;
+            meta->pass_count += 1;
+            meta->avail = end ? (uint64_t)NA * N - 1 - emit_n : 0;
+        }
+        grid_barrier(gbar, epoch);
+        if (emit_n) {
+            // natural index m*N + jh*C + jl is stored at m*N + jl*R + jh
+            const uint32_t tiles_h = (R + kRunTile - 1) / kRunTile;
+            const uint32_t tiles_l = (C + kRunTile - 1) / kRunTile;
+            const uint32_t ntiles = tiles_h * tiles_l * NA;
+            char* outc = static_cast<char*>(a.out) + run.out_off[i] * (a.out_f32 ? 4 : 8);
+            const uint32_t tx = t & 31u, ty = t >> 5;  // 32 x 16
+            // the next tile's 8 values per thread load while this one is stored
+            auto tile_at = [&](uint32_t tl, uint32_t& m, uint32_t& jh0, uint32_t& jl0) {
+                m = tl / (tiles_h * tiles_l);
+                const uint32_t rem = tl - m * tiles_h * tiles_l;
+                jh0 = (rem % tiles_h) * kRunTile;
+                jl0 = (rem / tiles_h) * kRunTile;
+            };
+            auto load_tile = [&](uint32_t tl, T (&v)[8]) {
+                uint32_t m, jh0, jl0;
+                tile_at(tl, m, jh0, jl0);
+                const T* pool = dpool + (uint64_t)m * N;
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k)
+#pragma unroll
+                    for (uint32_t h = 0; h < 2; ++h) {
+                        const uint32_t jl = jl0 + ty + 16 * k, jh = jh0 + tx + 32 * h;
+                        v[2 * k + h] = jl < C && jh < R ? pool[(uint64_t)jl * R + jh] : (T)0;
+                    }
+            };
+            T v[8];
+            if (blockIdx.x < ntiles) load_tile(blockIdx.x, v);
+            for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k)
+#pragma unroll
+                    for (uint32_t h = 0; h < 2; ++h) tile[ty + 16 * k][tx + 32 * h] = v[2 * k + h];
+                __syncthreads();
+                if (tl + gridDim.x < ntiles) load_tile(tl + gridDim.x, v);
+                uint32_t m, jh0, jl0;
+                tile_at(tl, m, jh0, jl0);
+                const uint64_t mbase = (uint64_t)m * N;
+#pragma unroll
+                for (uint32_t k = 0; k < kRunTile; k += 16) {
+                    const uint32_t jh = jh0 + ty + k;
+#pragma unroll
+                    for (uint32_t h = 0; h < kRunTile; h += 32) {
+                        const uint32_t jl = jl0 + tx + h;
+                        const uint64_t flat = mbase + (uint64_t)jh * C + jl;
+                        if (jl < C && jh < R && flat < emit_n)
+                            put_out_cs(outc, flat, tile[tx + h][ty + k], a.out_f32, a.unit,
+                                       a.mu, a.sigma);
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+}
+
+template <typename T, int NA>
+static cudaError_t hbm_run_go(const KernelArgs& a, wrng_gpu_params* params, const HbmRun& run,
+                              unsigned long long* gbar, cudaStream_t st) {
+    const HbmSplit sp = hbm_split(a.N);
+    const uint32_t R = 1u << sp.lr;
+    const size_t smem = (size_t)kRunStages * NA * R * sizeof(T) +
+                        (size_t)kRunTile * (kRunTile + 1) * sizeof(T);
+    auto kern = k_hbm_run<T, NA>;
+    static int occ_cache[2][2][64] = {};  // [dtype][n4][device] blocks per SM
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& occ = occ_cache[sizeof(T) == 8][NA == 4][dev & 63];
+    if (occ == 0) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        int nb = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kRunThreads, smem);
+        if (e != cudaSuccess) return e;
+        int sms = 0;
+        e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return e;
+        occ = nb * sms;
+        if (occ <= 0) return cudaErrorLaunchOutOfResources;
+    }
+    cudaError_t e = cudaMemsetAsync(gbar, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)occ);
+    cfg.blockDim = dim3(kRunThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeCooperative;  // co-residency for grid_barrier
+    attr[na].val.cooperative = 1;
+    ++na;
+    if (a.l2_bytes) {
+        attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[na].val.accessPolicyWindow.base_ptr = a.l2_base;
+        attr[na].val.accessPolicyWindow.num_bytes = a.l2_bytes;
+        attr[na].val.accessPolicyWindow.hitRatio = a.l2_hit;
+        attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, kern, a, params, run, gbar);
+}
+
+cudaError_t launch_hbm_run(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
+                           wrng_gpu_params* params, const HbmRun& run, unsigned long long* gbar,
+                           cudaStream_t st) {
+    if (run.npass == 0) return cudaSuccess;
+    if (dtype == WRNG_GPU_F64)
+        return n_arrays == 2 ? hbm_run_go<double, 2>(a, params, run, gbar, st)
+                             : hbm_run_go<double, 4>(a, params, run, gbar, st);
+    return n_arrays == 2 ? hbm_run_go<float, 2>(a, params, run, gbar, st)
+                         : hbm_run_go<float, 4>(a, params, run, gbar, st);
+}
+
 }  // namespace wg
+

@@ -111,6 +111,21 @@ struct HbmPass {
     uint64_t out_off;    // ... to out + out_off
     uint32_t end_refill; // 1: last pass of a refill (sets avail = cap - emit_n)
 };
+// A run of consecutive passes (no drift audit, restart or leftover emission
+// in between) executed by ONE persistent launch with grid-wide barriers
+// between passes (k_hbm_run).  Pass i reads buffer src0 ^ (i & 1) and uses
+// params[param0 + i]; emit_n[i] > 0 streams the new pool's flat [0, emit_n)
+// to out + out_off[i].
+constexpr uint32_t kRunMax = 64;
+struct HbmRun {
+    uint32_t npass, src0, param0, pad_;
+    uint64_t end_mask;  // bit i: pass i ends a refill
+    uint64_t emit_n[kRunMax];
+    uint64_t out_off[kRunMax];
+};
+cudaError_t launch_hbm_run(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
+                           wrng_gpu_params* params, const HbmRun& run, unsigned long long* gbar,
+                           cudaStream_t st);
 cudaError_t launch_hbm_params(uint32_t n_arrays, uint32_t N, LfgState* lfg,
                               wrng_gpu_params* params, uint32_t npass, PoolMeta* meta,
                               cudaStream_t st);
