@@ -382,6 +382,62 @@ def test_cluster_engine_matches_oracle(W, n, dt, p):
     assert r.stdout.strip().splitlines()[-1] == "OK"
 
 
+@pytest.mark.parametrize("n,dt,p,f,drift,restart", [
+    (4, "f64", 15, 2, 0, 0),   # no audits: runs split only at 64 passes
+    (2, "f32", 16, 3, 5, 0),   # audits split the runs
+    (4, "f32", 14, 1, 3, 7),   # restarts inside the fill
+])
+def test_hbm_persistent_runs_match_oracle(W, n, dt, p, f, drift, restart):
+    """HBM pools with many storage rows (C = N / 512 up to 128): the
+    persistent run kernel (grid barrier between passes, TMA row pipeline,
+    emission tiles) is bit-identical to the oracle for long fills, leftover
+    windows, partial refills and generic (mu, sigma / other width) output."""
+    kw = dict(pool_exponent=p, throwaway_f=f, seed=77, n_arrays=n, dtype=dt,
+              drift_check_period=drift, restart_interval_passes=restart)
+    g = gpu_state(W, init_on_host=True, force_hbm=True, **kw)
+    assert g.engine() == "hbm"
+    o = oracle_state(**kw)
+    cap = n * (1 << p) - 1
+    for cnt in (70 * cap + 3, 5, 2 * cap - 7):
+        assert_bits(g.fill(cnt), o.fill(cnt))
+    other = "f32" if dt == "f64" else "f64"
+    onp = np.float32 if other == "f32" else np.float64
+    assert_bits(g.fill(3 * cap + 1, 0.5, 2.0), o.fill(3 * cap + 1, 0.5, 2.0))
+    assert_bits(g.fill(2 * cap, dtype=other), o.fill(2 * cap, out_dtype=onp))
+    pv, pt, pw = o.pool()
+    gp = g.active_pool()
+    assert np.array_equal(gp.arrays.reshape(-1).astype(np.float64), pv)
+    assert (gp.tracked_sumsq, gp.withheld) == (pt, pw)
+
+
+def test_hbm_run_and_stepwise_paths_agree(W):
+    """WRNG_GPU_HBM_STEPWISE=1 (one launch per pass and per emission) and the
+    default persistent runs give the same bits (subprocess: the switch is
+    read when the library loads)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, hashlib\n"
+        "import paper_1004_3114_b200 as W\n"
+        "g = W.WallaceState(W.WallaceConfig(pool_exponent=17, throwaway_f=2, seed=9, n_arrays=4,"
+        " dtype='f64', drift_check_period=6, force_hbm=True))\n"
+        "h = hashlib.sha256()\n"
+        "for c in (40 * 4 * 2**17 + 9, 17, 4 * 2**17):\n"
+        "    h.update(g.fill(c).tobytes())\n"
+        "p = g.active_pool()\n"
+        "h.update(p.arrays.tobytes()); h.update(np.array([p.tracked_sumsq, p.withheld]).tobytes())\n"
+        "print(h.hexdigest())\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ({}, {"WRNG_GPU_HBM_STEPWISE": "1"}):
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, **env),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        outs.append(r.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1]
+
+
 def test_host_fill_larger_than_staging(W):
     """Host output larger than the 2 x 256 MiB staging slabs (f32 bank)."""
     g = gpu_state(W, pool_exponent=10, throwaway_f=1, seed=31, n_arrays=4, dtype="f32", pools=148,
