@@ -743,6 +743,9 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned l
     __syncthreads();
 }
 
+#ifndef WG_RUN_EMIT_OVERLAP
+#define WG_RUN_EMIT_OVERLAP 1
+#endif
 constexpr uint32_t kRunThreads = 512;
 constexpr uint32_t kRunTile = 64;
 constexpr uint32_t kRunStages = 3;  // source-row buffers in flight per CTA
@@ -798,8 +801,71 @@ __global__ void __launch_bounds__(kRunThreads, 2)
     __syncthreads();
     uint32_t q = 0;  // source rows consumed by this CTA so far (stage q % S)
     unsigned long long epoch = 0;  // grid barrier target
+    // Emission of a freshly regenerated pool (wallace.cpp:206-213), streamed
+    // by all CTAs in 64 x 64 transpose tiles; it runs after the NEXT pass's
+    // row loads and scale are issued, so those overlap it (both only read
+    // the new pool).
+    auto emit = [&](const T* e_pool, uint64_t e_n, uint64_t e_off) {
+        // natural index m*N + jh*C + jl is stored at m*N + jl*R + jh
+        const uint32_t tiles_h = (R + kRunTile - 1) / kRunTile;
+        const uint32_t tiles_l = (C + kRunTile - 1) / kRunTile;
+        const uint32_t ntiles = tiles_h * tiles_l * NA;
+        char* outc = static_cast<char*>(a.out) + e_off * (a.out_f32 ? 4 : 8);
+        const uint32_t tx = t & 31u, ty = t >> 5;  // 32 x 16
+        // the next tile's 8 values per thread load while this one is stored
+        auto tile_at = [&](uint32_t tl, uint32_t& m, uint32_t& jh0, uint32_t& jl0) {
+            m = tl / (tiles_h * tiles_l);
+            const uint32_t rem = tl - m * tiles_h * tiles_l;
+            jh0 = (rem % tiles_h) * kRunTile;
+            jl0 = (rem / tiles_h) * kRunTile;
+        };
+        auto load_tile = [&](uint32_t tl, T (&v)[8]) {
+            uint32_t m, jh0, jl0;
+            tile_at(tl, m, jh0, jl0);
+            const T* pool = e_pool + (uint64_t)m * N;
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k)
+#pragma unroll
+                for (uint32_t h = 0; h < 2; ++h) {
+                    const uint32_t jl = jl0 + ty + 16 * k, jh = jh0 + tx + 32 * h;
+                    v[2 * k + h] = jl < C && jh < R ? pool[(uint64_t)jl * R + jh] : (T)0;
+                }
+        };
+        T v[8];
+        if (blockIdx.x < ntiles) load_tile(blockIdx.x, v);
+        for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k)
+#pragma unroll
+                for (uint32_t h = 0; h < 2; ++h) tile[ty + 16 * k][tx + 32 * h] = v[2 * k + h];
+            __syncthreads();
+            if (tl + gridDim.x < ntiles) load_tile(tl + gridDim.x, v);
+            uint32_t m, jh0, jl0;
+            tile_at(tl, m, jh0, jl0);
+            const uint64_t mbase = (uint64_t)m * N;
+#pragma unroll
+            for (uint32_t k = 0; k < kRunTile; k += 16) {
+                const uint32_t jh = jh0 + ty + k;
+#pragma unroll
+                for (uint32_t h = 0; h < kRunTile; h += 32) {
+                    const uint32_t jl = jl0 + tx + h;
+                    const uint64_t flat = mbase + (uint64_t)jh * C + jl;
+                    if (jl < C && jh < R && flat < e_n)
+                        put_out_cs(outc, flat, tile[tx + h][ty + k], a.out_f32, a.unit,
+                                   a.mu, a.sigma);
+                }
+            }
+            __syncthreads();
+        }
+    };
+    const T* pend_pool = nullptr;  // emission owed by the previous pass
+    uint64_t pend_n = 0, pend_off = 0;
 
     for (uint32_t i = 0; i < run.npass; ++i) {
+        if (!WG_RUN_EMIT_OVERLAP && pend_n) {  // A/B: emission before the next pass's setup
+            emit(pend_pool, pend_n, pend_off);
+            pend_n = 0;
+        }
         const uint32_t src = run.src0 ^ (i & 1u), dst = src ^ 1u;
         const wrng_gpu_params prm = params[run.param0 + i];
         const T* spool = static_cast<const T*>(a.buf[src]);
@@ -838,6 +904,10 @@ __global__ void __launch_bounds__(kRunThreads, 2)
                 }
             }
             s_err = err;
+        }
+        if (pend_n) {
+            emit(pend_pool, pend_n, pend_off);
+            pend_n = 0;
         }
         __syncthreads();
         if (s_err) {  // every CTA reads the same state: all leave here together
@@ -905,59 +975,12 @@ __global__ void __launch_bounds__(kRunThreads, 2)
         }
         grid_barrier(gbar, epoch);
         if (emit_n) {
-            // natural index m*N + jh*C + jl is stored at m*N + jl*R + jh
-            const uint32_t tiles_h = (R + kRunTile - 1) / kRunTile;
-            const uint32_t tiles_l = (C + kRunTile - 1) / kRunTile;
-            const uint32_t ntiles = tiles_h * tiles_l * NA;
-            char* outc = static_cast<char*>(a.out) + run.out_off[i] * (a.out_f32 ? 4 : 8);
-            const uint32_t tx = t & 31u, ty = t >> 5;  // 32 x 16
-            // the next tile's 8 values per thread load while this one is stored
-            auto tile_at = [&](uint32_t tl, uint32_t& m, uint32_t& jh0, uint32_t& jl0) {
-                m = tl / (tiles_h * tiles_l);
-                const uint32_t rem = tl - m * tiles_h * tiles_l;
-                jh0 = (rem % tiles_h) * kRunTile;
-                jl0 = (rem / tiles_h) * kRunTile;
-            };
-            auto load_tile = [&](uint32_t tl, T (&v)[8]) {
-                uint32_t m, jh0, jl0;
-                tile_at(tl, m, jh0, jl0);
-                const T* pool = dpool + (uint64_t)m * N;
-#pragma unroll
-                for (uint32_t k = 0; k < 4; ++k)
-#pragma unroll
-                    for (uint32_t h = 0; h < 2; ++h) {
-                        const uint32_t jl = jl0 + ty + 16 * k, jh = jh0 + tx + 32 * h;
-                        v[2 * k + h] = jl < C && jh < R ? pool[(uint64_t)jl * R + jh] : (T)0;
-                    }
-            };
-            T v[8];
-            if (blockIdx.x < ntiles) load_tile(blockIdx.x, v);
-            for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-#pragma unroll
-                for (uint32_t k = 0; k < 4; ++k)
-#pragma unroll
-                    for (uint32_t h = 0; h < 2; ++h) tile[ty + 16 * k][tx + 32 * h] = v[2 * k + h];
-                __syncthreads();
-                if (tl + gridDim.x < ntiles) load_tile(tl + gridDim.x, v);
-                uint32_t m, jh0, jl0;
-                tile_at(tl, m, jh0, jl0);
-                const uint64_t mbase = (uint64_t)m * N;
-#pragma unroll
-                for (uint32_t k = 0; k < kRunTile; k += 16) {
-                    const uint32_t jh = jh0 + ty + k;
-#pragma unroll
-                    for (uint32_t h = 0; h < kRunTile; h += 32) {
-                        const uint32_t jl = jl0 + tx + h;
-                        const uint64_t flat = mbase + (uint64_t)jh * C + jl;
-                        if (jl < C && jh < R && flat < emit_n)
-                            put_out_cs(outc, flat, tile[tx + h][ty + k], a.out_f32, a.unit,
-                                       a.mu, a.sigma);
-                    }
-                }
-                __syncthreads();
-            }
+            pend_pool = dpool;
+            pend_n = emit_n;
+            pend_off = run.out_off[i];
         }
     }
+    if (pend_n) emit(pend_pool, pend_n, pend_off);
 }
 
 template <typename T, int NA>
