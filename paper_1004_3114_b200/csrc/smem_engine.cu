@@ -57,8 +57,7 @@ bool smem_engine_fits(uint32_t n_arrays, uint32_t dtype, uint32_t N) {
 EngineShape smem_engine_shape(uint32_t n_arrays, uint32_t dtype, uint32_t N) {
     const uint32_t es = dtype == WRNG_GPU_F64 ? 8 : 4;
     EngineShape s;
-    s.j = pick_j(N, n_arrays * es / 4,
-                 es == 4 && n_arrays == 4 ? WG_DATA_REGS_F32N4 : WG_DATA_REGS);
+    s.j = pick_j(N, n_arrays * es / 4, WG_DATA_REGS);
     s.threads = N / s.j;
     s.smem = 0;
     return s;
