@@ -990,17 +990,21 @@ static cudaError_t hbm_run_go(const KernelArgs& a, wrng_gpu_params* params, cons
     const uint32_t R = 1u << sp.lr;
     const size_t smem = (size_t)kRunStages * NA * R * sizeof(T) +
                         (size_t)kRunTile * (kRunTile + 1) * sizeof(T);
+    // attribute and occupancy for the largest row length (R = 512), so one
+    // cached grid size is co-resident for every pool size
+    const size_t smem_max = (size_t)kRunStages * NA * 512 * sizeof(T) +
+                            (size_t)kRunTile * (kRunTile + 1) * sizeof(T);
     auto kern = k_hbm_run<T, NA>;
-    static int occ_cache[2][2][64] = {};  // [dtype][n4][device] blocks per SM
+    static int occ_cache[2][2][64] = {};  // [dtype][n4][device] CTAs in the grid
     int dev = 0;
     cudaGetDevice(&dev);
     int& occ = occ_cache[sizeof(T) == 8][NA == 4][dev & 63];
     if (occ == 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+                                             (int)smem_max);
         if (e != cudaSuccess) return e;
         int nb = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kRunThreads, smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kRunThreads, smem_max);
         if (e != cudaSuccess) return e;
         int sms = 0;
         e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -438,6 +438,32 @@ def test_hbm_run_and_stepwise_paths_agree(W):
     assert outs[0] == outs[1]
 
 
+def test_hbm_run_small_then_large_pool_in_one_process(W):
+    """The run kernel's cached grid must suit every pool size: a small forced
+    HBM pool first (short rows), then a large one, in a fresh process."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, sys\n"
+        "sys.path.insert(0, 'oracle')\n"
+        "import oracle as O\n"
+        "import paper_1004_3114_b200 as W\n"
+        "ok = True\n"
+        "for p in (8, 16):\n"
+        "    kw = dict(pool_exponent=p, throwaway_f=2, seed=5, n_arrays=4, dtype='f64')\n"
+        "    g = W.WallaceState(W.WallaceConfig(init_on_host=True, force_hbm=True, **kw))\n"
+        "    o = O.OracleState(pool_exponent=p, throwaway_f=2, seed=5, n_arrays=4, dtype=O.F64)\n"
+        "    c = 3 * 4 * 2**p + 11\n"
+        "    ok &= bool(np.array_equal(g.fill(c), o.fill(c)))\n"
+        "print('OK' if ok else 'MISMATCH')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.strip().splitlines()[-1] == "OK"
+
+
 def test_host_fill_larger_than_staging(W):
     """Host output larger than the 2 x 256 MiB staging slabs (f32 bank)."""
     g = gpu_state(W, pool_exponent=10, throwaway_f=1, seed=31, n_arrays=4, dtype="f32", pools=148,
