@@ -357,7 +357,10 @@ cudaError_t launch_hbm_emit(uint32_t, uint32_t dtype, const KernelArgs& a, uint3
 // tree != 0: blocked parallel reduction (documented deviation, relative
 // error ~1e-16 * log n).
 // ---------------------------------------------------------------------------
-constexpr uint32_t kSumChunk = 128;
+#ifndef WG_SUM_CHUNK
+#define WG_SUM_CHUNK 64  // terms per chunk (C2: 64 -> 9.36 ms/step, 128 -> 9.59, 32 -> 9.43)
+#endif
+constexpr uint32_t kSumChunk = WG_SUM_CHUNK;
 constexpr uint32_t kSumCta = 256;  // chunks per CTA of kernels 1-2
 
 template <typename T>
