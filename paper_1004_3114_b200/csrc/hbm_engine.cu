@@ -768,6 +768,28 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+#ifndef WG_RUN_L2HINT  // 1: source rows evict_first, new pool rows evict_last
+#define WG_RUN_L2HINT 0
+#endif
+// global -> shared bulk copy completing on an mbarrier (TMA, 1-D), with an
+// L2 cache policy
+__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes,
+                                              uint32_t bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
+template <typename T>
+__device__ __forceinline__ void st_hint(T* p, T v, uint64_t pol) {
+    if constexpr (sizeof(T) == 8)
+        asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol)
+                     : "memory");
+    else
+        asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol)
+                     : "memory");
+}
 // global -> shared bulk copy completing on an mbarrier (TMA, 1-D)
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
                                          uint32_t bar) {
@@ -802,6 +824,11 @@ __global__ void __launch_bounds__(kRunThreads, 2)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    uint64_t pol_first = 0, pol_last = 0;
+    if (WG_RUN_L2HINT) {
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+    }
     uint32_t q = 0;  // source rows consumed by this CTA so far (stage q % S)
     unsigned long long epoch = 0;  // grid barrier target
     // Emission of a freshly regenerated pool (wallace.cpp:206-213), streamed
@@ -884,8 +911,13 @@ __global__ void __launch_bounds__(kRunThreads, 2)
 #pragma unroll
             for (int m = 0; m < NA; ++m) {
                 const uint32_t srow = (prm.stride[m] * jlo + prm.offset[m]) & (C - 1);
-                bulk_g2s(stage_s + (sb * NA + m) * row_bytes,
-                         spool + (uint64_t)m * N + (uint64_t)srow * R, row_bytes, bar);
+                if (WG_RUN_L2HINT)
+                    bulk_g2s_hint(stage_s + (sb * NA + m) * row_bytes,
+                                  spool + (uint64_t)m * N + (uint64_t)srow * R, row_bytes, bar,
+                                  pol_first);
+                else
+                    bulk_g2s(stage_s + (sb * NA + m) * row_bytes,
+                             spool + (uint64_t)m * N + (uint64_t)srow * R, row_bytes, bar);
             }
         };
         if (t == 0) {
@@ -957,7 +989,12 @@ __global__ void __launch_bounds__(kRunThreads, 2)
                     }
                 }
 #pragma unroll
-                for (int m = 0; m < NA; ++m) dpool[(uint64_t)m * N + (uint64_t)jlo * R + t] = y[m];
+                for (int m = 0; m < NA; ++m) {
+                    if (WG_RUN_L2HINT)
+                        st_hint(dpool + (uint64_t)m * N + (uint64_t)jlo * R + t, y[m], pol_last);
+                    else
+                        dpool[(uint64_t)m * N + (uint64_t)jlo * R + t] = y[m];
+                }
                 if (jlo == C - 1 && t == R - 1) meta->withheld[dst] = (double)y[NA - 1];
             }
             __syncthreads();  // stage sb fully read
