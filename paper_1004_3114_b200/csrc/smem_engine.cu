@@ -9,6 +9,8 @@ cudaError_t smem_dispatch_f32_n2(const KernelArgs&, cudaStream_t, bool, bool);
 cudaError_t smem_dispatch_f32_n4(const KernelArgs&, cudaStream_t, bool, bool);
 cudaError_t smem_dispatch_f64_n2(const KernelArgs&, cudaStream_t, bool, bool);
 cudaError_t smem_dispatch_f64_n4(const KernelArgs&, cudaStream_t, bool, bool);
+bool smem_r64_fits(uint32_t dtype, uint32_t N);
+cudaError_t smem_dispatch_n4_r64(uint32_t dtype, const KernelArgs&, cudaStream_t, bool, bool);
 
 __global__ void k_smem_base_probe(uint32_t* out) {
     if (threadIdx.x == 0) *out = (uint32_t)__cvta_generic_to_shared(g_sm) & 0xFFFFFFu;
@@ -68,6 +70,10 @@ cudaError_t launch_smem(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
     const bool unit_same =
         a.op != OP_FILL || (a.unit && (a.out_f32 != 0) == (dtype == WRNG_GPU_F32));
     const bool al = aligned_layout_ok();
+    // f >= 2 on small n = 4 pools: the 64-register engine (two warps per
+    // 4x1024 fp32 pool) — non-emitting passes are generation-bound
+    if (n_arrays == 4 && a.op == OP_FILL && a.f >= 2 && smem_r64_fits(dtype, a.N))
+        return smem_dispatch_n4_r64(dtype, a, st, unit_same, al);
     if (dtype == WRNG_GPU_F64)
         return n_arrays == 2 ? smem_dispatch_f64_n2(a, st, unit_same, al)
                              : smem_dispatch_f64_n4(a, st, unit_same, al);

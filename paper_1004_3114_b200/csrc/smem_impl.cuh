@@ -47,7 +47,15 @@
 #define WG_DATA_REGS 128
 #endif
 
+// Each translation unit instantiates the engine in its own namespace, so a
+// second register budget (WG_DATA_REGS, e.g. 64 in smem_*_r64.cu) can live
+// beside the default one.
+#ifndef WG_SMEM_NS
+#define WG_SMEM_NS r128
+#endif
+
 namespace wg {
+namespace WG_SMEM_NS {
 
 static constexpr uint32_t kSmemPoolMax = 128 * 1024;  // largest pool kept on chip
 
@@ -981,4 +989,6 @@ static cudaError_t dispatch(const KernelArgs& a, cudaStream_t st, bool unit_same
     }
 }
 
+}  // namespace WG_SMEM_NS
+using namespace WG_SMEM_NS;
 }  // namespace wg
