@@ -327,7 +327,26 @@ wrng_gpu_status run_hbm(wrng_gpu* g, uint32_t p, Ctr c, const std::vector<Ev>& e
                     ++k;
                 }
                 --k;
-                LAUNCH(launch_hbm_run(NA, dt, a, g->params, run, g->gbar, s));
+                cudaError_t re = launch_hbm_run(NA, dt, a, g->params, run, g->gbar, s);
+                if (re == cudaErrorCooperativeLaunchTooLarge || re == cudaErrorNotSupported) {
+                    // the device cannot co-schedule the grid (e.g. shared by
+                    // another context): the same passes, one launch each
+                    (void)cudaGetLastError();
+                    for (uint32_t r = 0; r < run.npass; ++r) {
+                        HbmPass ps{};
+                        ps.src = run.src0 ^ (r & 1u);
+                        ps.param_idx = run.param0 + r;
+                        ps.emit_n = run.emit_n[r];
+                        ps.out_off = run.out_off[r];
+                        ps.end_refill = (uint32_t)((run.end_mask >> r) & 1u);
+                        LAUNCH(launch_hbm_pass(NA, dt, a, g->params, ps, s));
+                        if (ps.emit_n)
+                            LAUNCH(launch_hbm_emit_t(NA, dt, a, ps.src ^ 1u, ps.emit_n,
+                                                     ps.out_off, s));
+                    }
+                    continue;
+                }
+                LAUNCH(re);
                 continue;
             }
             if (e.kind == Ev::EMIT) {
