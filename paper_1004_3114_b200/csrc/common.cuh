@@ -273,7 +273,7 @@ __device__ __forceinline__ void draw_pass_params_warp(uint64_t* tab, Ctl* ctl, u
     } else {
         // strides from {3,5}, {7,11}, {13,17}, {19,23} (docs/n4_spec.md §2)
         if (lane < 4) {
-            const uint32_t lo = lane == 0 ? 3 : lane == 1 ? 7 : lane == 2 ? 13 : 19;
+            const uint32_t lo = (0x130D0703u >> (8u * lane)) & 0xFFu;  // 3, 7, 13, 19
             p.stride[lane] = nib_pow2(w, 1) == 0 ? lo : lo + (lane == 0 ? 2 : 4);
         } else if (lane < 8) {
             p.offset[lane - 4] = nib_pow2(w, (uint32_t)__ffs(N) - 1);
@@ -314,7 +314,8 @@ __device__ __forceinline__ void draw_pass_params_all(uint64_t* tab, Ctl* ctl, ui
         const bool mine = lane < K;
         const uint64_t w = mine ? tab[i] + tab[s] : 0ull;
         if (writer && mine) tab[i] = w;
-        const uint32_t lo = lane == 0 ? 3u : lane == 1 ? 7u : lane == 2 ? 13u : 19u;
+        // 3, 7, 13, 19 for lanes 0..3 without a per-lane jump table
+        const uint32_t lo = (0x130D0703u >> (8u * (lane & 3u))) & 0xFFu;
         const uint32_t strd = (w >> 63) ? lo + (lane == 0 ? 2u : 4u) : lo;
         const uint32_t offs = (uint32_t)(w >> (64 - ((uint32_t)__ffs(N) - 1)));
         const uint32_t val = lane < 4 ? strd : lane < 8 ? offs : (uint32_t)(w >> 63);
