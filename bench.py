@@ -366,28 +366,27 @@ def main():
                 "kernel_ms": kernel_ms}
 
     # ---- e2e: same public call, HOST output (pinned), bounded sample -------
-    e2e = None
-    if rank == 0 or True:
-        # per-rank pinned host buffer: 4 GiB at N = 1, 1 GiB per rank at N > 1
-        n_e2e = min(args.e2e_sample if world == 1 else min(args.e2e_sample, 1 << 28), per_gpu)
-        host = torch.empty(n_e2e, dtype=out_dtype, pin_memory=True)
-        hv = host.numpy()
-        gen.fill(hv)  # warm (allocates staging)
-        t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            gen.fill(hv)
-        t1 = time.perf_counter()
-        e2e_local = n_e2e * args.e2e_steps / (t1 - t0)
-        if world > 1:
-            t = torch.tensor([t1 - t0], device=dev, dtype=torch.float64)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_local = n_e2e * args.e2e_steps * world / float(t.item())
-        e2e = {"value": e2e_local, "unit": UNIT, "h2d_bytes_per_step": 0,
-               "d2h_bytes_per_step": n_e2e * esize,
-               "sample": f"{n_e2e} normals per rank per step into pinned host memory via "
-                         f"wrng_gpu_fill_{c['dtype']}(out_is_device=0); generator state is "
-                         f"device-resident, so no host->device input bytes"}
-        del host
+    # every rank runs it; at N > 1 the slowest rank's time counts
+    # per-rank pinned host buffer: 4 GiB at N = 1, 1 GiB per rank at N > 1
+    n_e2e = min(args.e2e_sample if world == 1 else min(args.e2e_sample, 1 << 28), per_gpu)
+    host = torch.empty(n_e2e, dtype=out_dtype, pin_memory=True)
+    hv = host.numpy()
+    gen.fill(hv)  # warm (allocates staging)
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        gen.fill(hv)
+    t1 = time.perf_counter()
+    e2e_local = n_e2e * args.e2e_steps / (t1 - t0)
+    if world > 1:
+        t = torch.tensor([t1 - t0], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_local = n_e2e * args.e2e_steps * world / float(t.item())
+    e2e = {"value": e2e_local, "unit": UNIT, "h2d_bytes_per_step": 0,
+           "d2h_bytes_per_step": n_e2e * esize,
+           "sample": f"{n_e2e} normals per rank per step into pinned host memory via "
+                     f"wrng_gpu_fill_{c['dtype']}(out_is_device=0); generator state is "
+                     f"device-resident, so no host->device input bytes"}
+    del host
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
