@@ -13,6 +13,10 @@
 //   mode 7: as 1 but CTA p starts at chunk (37 p) mod nchunks (decorrelated)
 //   mode 8+: bulk, aligned chunks of CB bytes, P2 CTAs, queue Q, optional
 //            L2 evict_first hint (see table in main)
+//   mode 23: C3's actual emission: per refill 4 bulk copies (one per 1024-value
+//            array, 64 B-aligned spans) + warp stores of the ragged values
+//   mode 24: as 23 but ONE bulk copy per refill (64 B-aligned interior of
+//            the whole 4095-value window) + warp stores of its ragged ends
 //   mode 16+: C3's exact segments and refill boundaries (4095 values), but
 //            each refill's copy is [first U-aligned byte of the not yet
 //            written part, last U-aligned byte of the refill): what a
@@ -156,6 +160,49 @@ __global__ void __launch_bounds__(64) k_bulk_carry(float* out, uint64_t seg, uin
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// one warp per CTA, like the one-warp C3 pools
+template <int ONE>
+__global__ void __launch_bounds__(32) k_c3_emit(float* out, uint64_t seg) {
+    extern __shared__ __align__(1024) float sm[];
+    for (int i = threadIdx.x; i < 4096 + 64; i += 32) sm[i] = (float)blockIdx.x;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    float* o = out + (uint64_t)blockIdx.x * seg;
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(sm);
+    const uint32_t lane = threadIdx.x;
+    for (uint64_t done = 0; done < seg; done += kChunk) {
+        const uint64_t n = seg - done < kChunk ? seg - done : kChunk;
+        float* w = o + done;
+        const uint32_t nspan = ONE ? 1 : 4;
+        for (uint32_t m = 0; m < nspan; ++m) {
+            const uint64_t lo = ONE ? 0 : m * 1024ull;
+            const uint64_t hi = ONE || m == 3 || (m + 1) * 1024ull > n ? n : (m + 1) * 1024ull;
+            if (hi <= lo) continue;
+            uint64_t a = reinterpret_cast<uint64_t>(w + lo);
+            uint64_t e = reinterpret_cast<uint64_t>(w + hi);
+            const uint64_t a64 = (a + 63) & ~63ull, e64 = e & ~63ull;
+            // ragged head [a, a64) and tail [e64, e): warp stores
+            const uint32_t nh = (uint32_t)((a64 > e ? e : a64) - a) / 4;
+            if (lane < nh) w[lo + lane] = 1.0f;
+            if (e64 > a64) {
+                const uint32_t nt = (uint32_t)(e - e64) / 4;
+                if (lane < nt) reinterpret_cast<float*>(e64)[lane] = 1.0f;
+                if (lane == 0) {
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(a64),
+                                 "r"(s), "r"((uint32_t)(e64 - a64))
+                                 : "memory");
+                }
+            }
+        }
+        if (lane == 0) {
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        __syncwarp();
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __global__ void k_fill8(float* out, uint64_t n8) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n8;
          i += (uint64_t)gridDim.x * blockDim.x)
@@ -208,7 +255,27 @@ int main(int argc, char** argv) {
     cudaFuncSetAttribute(k_bulk_carry, cudaFuncAttributeMaxDynamicSharedMemorySize, 36864);
     const int nmodes = argc > 2 ? atoi(argv[2]) : 16;
     const uint32_t carry_u[] = {16, 128, 512, 1024, 2048, 4096, 16384};
-    for (int mode = 0; mode < nmodes; ++mode) {
+    cudaFuncSetAttribute(k_c3_emit<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 17000);
+    cudaFuncSetAttribute(k_c3_emit<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 17000);
+    const int first = argc > 3 ? atoi(argv[3]) : 0;
+    for (int mode = first; mode < nmodes; ++mode) {
+        if (mode >= 23) {
+            float best = 1e30f;
+            for (int rep = 0; rep < 5; ++rep) {
+                cudaEventRecord(a);
+                if (mode == 23) k_c3_emit<0><<<P, 32, 17000>>>(out, seg);
+                else k_c3_emit<1><<<P, 32, 17000>>>(out, seg);
+                cudaEventRecord(b);
+                cudaEventSynchronize(b);
+                float ms = 0;
+                cudaEventElapsedTime(&ms, a, b);
+                if (rep > 0 && ms < best) best = ms;
+            }
+            cudaError_t e = cudaGetLastError();
+            printf("{\"mode\": %d, \"ms\": %.3f, \"gbs\": %.1f, \"err\": \"%s\"}\n", mode, best,
+                   (double)(P * seg) * 4 / (best / 1e3) / 1e9, cudaGetErrorString(e));
+            continue;
+        }
         if (mode >= 16) {
             const uint32_t ub = carry_u[(mode - 16) % 7];
             float best = 1e30f;
