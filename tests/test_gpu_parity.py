@@ -561,6 +561,72 @@ def test_fixed_mode_conserves_sum(W):
     assert abs(g.active_pool().direct_sumsq() / q0 - 1) <= 1e-12
 
 
+@pytest.mark.parametrize("n,bound", [(2, 2 ** 0.5), (4, 2.0)])
+def test_outlier_band_fixed_mode(W, n, bound):
+    """acceptance.cpp:207-220 on the GPU: with the sum of squares fixed, one
+    pass moves the largest |value| by at most the transform's norm bound
+    (sqrt 2 for the n = 2 rotation; 2 for the n = 4 matrices, whose rows
+    have four entries of size 1/2 or 1/2 and 1/2-1), over 1000 passes."""
+    g = gpu_state(W, pool_exponent=10, throwaway_f=1, seed=7, scale_mode=W.ScaleMode.fixed,
+                  n_arrays=n)
+    before = g.active_pool().max_abs()
+    for _ in range(1000):
+        g.advance_pass()
+        after = g.active_pool().max_abs()
+        eps = 1e-12 * before
+        assert before / bound - eps <= after <= bound * before + eps
+        before = after
+
+
+def test_threaded_independent_streams(W):
+    """test_wallace_state.cpp:175-191 on the GPU: three host threads, each
+    with its own generator (stream 0, 1, 2) and CUDA stream, fill at the
+    same time; each stream equals its sequential run, and they differ."""
+    import threading
+
+    def run(sid):
+        g = gpu_state(W, pool_exponent=10, throwaway_f=3, seed=0, stream_id=sid, n_arrays=4)
+        return g.fill(100000)
+
+    par = [None] * 3
+
+    def worker(i):
+        par[i] = run(i)
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for i in range(3):
+        assert_bits(par[i], run(i))
+    assert not np.array_equal(par[0], par[1])
+
+
+def test_cost_model_ratio_on_gpu(W):
+    """acceptance.cpp:222-230: t(f=3) / t(f=1) in [1.5, 4.5], here for the
+    C3-shaped bank (1184 fp32 n = 4 pools) on the device."""
+    import torch
+
+    out = torch.empty(1 << 28, dtype=torch.float32, device="cuda")
+    t = {}
+    for f in (1, 3):
+        g = gpu_state(W, pool_exponent=10, throwaway_f=f, seed=2024, n_arrays=4, dtype="f32",
+                      pools=1184)
+        g.fill(out)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        best = 1e30
+        for _ in range(3):
+            a.record()
+            g.fill(out)
+            b.record()
+            b.synchronize()
+            best = min(best, a.elapsed_time(b))
+        t[f] = best
+    assert 1.5 <= t[3] / t[1] <= 4.5, t
+
+
 def test_drift_check_raises_and_corrects(W):
     g = gpu_state(W, pool_exponent=10, throwaway_f=3, seed=1)
     g.refill()
