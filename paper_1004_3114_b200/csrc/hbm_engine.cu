@@ -746,8 +746,11 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned l
     __syncthreads();
 }
 
-#ifndef WG_RUN_EMIT_OVERLAP
-#define WG_RUN_EMIT_OVERLAP 1
+#ifndef WG_RUN_EMIT_MODE
+// where a refill's emission runs: 0 right after the barrier, 1 after the
+// next pass's row loads are issued, 2 after the next pass's rows, tiles
+// claimed dynamically (CTAs with fewer rows take more tiles)
+#define WG_RUN_EMIT_MODE 0
 #endif
 constexpr uint32_t kRunThreads = 512;
 constexpr uint32_t kRunTile = 64;
@@ -813,6 +816,7 @@ __global__ void __launch_bounds__(kRunThreads, 2)
     __shared__ __align__(8) uint64_t full[kRunStages];
     __shared__ double s_c0, s_c1, s_target, s_scale;
     __shared__ int s_err;
+    __shared__ uint32_t s_tile[2];
     PoolMeta* meta = a.meta;
     const uint32_t t = threadIdx.x;
     const bool active_t = t < R;  // R < 512 only for forced-HBM small pools
@@ -835,7 +839,7 @@ __global__ void __launch_bounds__(kRunThreads, 2)
     // by all CTAs in 64 x 64 transpose tiles; it runs after the NEXT pass's
     // row loads and scale are issued, so those overlap it (both only read
     // the new pool).
-    auto emit = [&](const T* e_pool, uint64_t e_n, uint64_t e_off) {
+    auto emit = [&](const T* e_pool, uint64_t e_n, uint64_t e_off, unsigned* ctr) {
         // natural index m*N + jh*C + jl is stored at m*N + jl*R + jh
         const uint32_t tiles_h = (R + kRunTile - 1) / kRunTile;
         const uint32_t tiles_l = (C + kRunTile - 1) / kRunTile;
@@ -861,15 +865,26 @@ __global__ void __launch_bounds__(kRunThreads, 2)
                     v[2 * k + h] = jl < C && jh < R ? pool[(uint64_t)jl * R + jh] : (T)0;
                 }
         };
+        // tiles: static (tl = blockIdx.x + k gridDim.x) or claimed from *ctr
+        auto next = [&](uint32_t cur, int slot) -> uint32_t {
+            if (!ctr) return cur + gridDim.x;
+            if (t == 0) s_tile[slot] = atomicAdd(ctr, 1u);
+            __syncthreads();
+            return s_tile[slot];
+        };
+        int slot = 0;
+        uint32_t tl = ctr ? next(0, slot) : blockIdx.x;
         T v[8];
-        if (blockIdx.x < ntiles) load_tile(blockIdx.x, v);
-        for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+        if (tl < ntiles) load_tile(tl, v);
+        while (tl < ntiles) {
 #pragma unroll
             for (uint32_t k = 0; k < 4; ++k)
 #pragma unroll
                 for (uint32_t h = 0; h < 2; ++h) tile[ty + 16 * k][tx + 32 * h] = v[2 * k + h];
             __syncthreads();
-            if (tl + gridDim.x < ntiles) load_tile(tl + gridDim.x, v);
+            slot ^= 1;
+            const uint32_t nt = next(tl, slot);
+            if (nt < ntiles) load_tile(nt, v);
             uint32_t m, jh0, jl0;
             tile_at(tl, m, jh0, jl0);
             const uint64_t mbase = (uint64_t)m * N;
@@ -886,14 +901,17 @@ __global__ void __launch_bounds__(kRunThreads, 2)
                 }
             }
             __syncthreads();
+            tl = nt;
         }
     };
     const T* pend_pool = nullptr;  // emission owed by the previous pass
     uint64_t pend_n = 0, pend_off = 0;
+    unsigned* pend_ctr = nullptr;
+    unsigned* tile_ctr = reinterpret_cast<unsigned*>(gbar + 1);  // [kRunMax], zeroed per launch
 
     for (uint32_t i = 0; i < run.npass; ++i) {
-        if (!WG_RUN_EMIT_OVERLAP && pend_n) {  // A/B: emission before the next pass's setup
-            emit(pend_pool, pend_n, pend_off);
+        if (WG_RUN_EMIT_MODE == 0 && pend_n) {
+            emit(pend_pool, pend_n, pend_off, nullptr);
             pend_n = 0;
         }
         const uint32_t src = run.src0 ^ (i & 1u), dst = src ^ 1u;
@@ -940,12 +958,13 @@ __global__ void __launch_bounds__(kRunThreads, 2)
             }
             s_err = err;
         }
-        if (pend_n) {
-            emit(pend_pool, pend_n, pend_off);
+        if (WG_RUN_EMIT_MODE == 1 && pend_n) {
+            emit(pend_pool, pend_n, pend_off, nullptr);
             pend_n = 0;
         }
         __syncthreads();
         if (s_err) {  // every CTA reads the same state: all leave here together
+            if (pend_n) emit(pend_pool, pend_n, pend_off, pend_ctr);  // the refill before stands
             // (rows already in flight complete into shared memory we abandon)
             if (t == 0)
                 for (uint32_t k = 0; k < nrows && k < kRunStages; ++k)
@@ -1003,6 +1022,10 @@ __global__ void __launch_bounds__(kRunThreads, 2)
                 issue(k + kRunStages);
             }
         }
+        if (WG_RUN_EMIT_MODE == 2 && pend_n) {
+            emit(pend_pool, pend_n, pend_off, pend_ctr);
+            pend_n = 0;
+        }
         const bool end = (run.end_mask >> i) & 1u;
         const uint64_t emit_n = run.emit_n[i];
         if (blockIdx.x == 0 && t == 0) {
@@ -1018,9 +1041,10 @@ __global__ void __launch_bounds__(kRunThreads, 2)
             pend_pool = dpool;
             pend_n = emit_n;
             pend_off = run.out_off[i];
+            pend_ctr = WG_RUN_EMIT_MODE == 2 ? tile_ctr + i : nullptr;
         }
     }
-    if (pend_n) emit(pend_pool, pend_n, pend_off);
+    if (pend_n) emit(pend_pool, pend_n, pend_off, pend_ctr);
 }
 
 template <typename T, int NA>
@@ -1052,7 +1076,8 @@ static cudaError_t hbm_run_go(const KernelArgs& a, wrng_gpu_params* params, cons
         occ = nb * sms;
         if (occ <= 0) return cudaErrorLaunchOutOfResources;
     }
-    cudaError_t e = cudaMemsetAsync(gbar, 0, sizeof(unsigned long long), st);
+    // barrier counter + the emission tile counters of this launch
+    cudaError_t e = cudaMemsetAsync(gbar, 0, kRunBarWords * sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)occ);

@@ -117,6 +117,9 @@ struct HbmPass {
 // params[param0 + i]; emit_n[i] > 0 streams the new pool's flat [0, emit_n)
 // to out + out_off[i].
 constexpr uint32_t kRunMax = 64;
+// k_hbm_run's device words: grid-barrier counter, then kRunMax 32-bit
+// emission tile counters (packed two per word)
+constexpr uint32_t kRunBarWords = 1 + kRunMax / 2;
 struct HbmRun {
     uint32_t npass, src0, param0, pad_;
     uint64_t end_mask;  // bit i: pass i ends a refill
