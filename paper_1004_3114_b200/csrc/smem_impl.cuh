@@ -333,7 +333,7 @@ __device__ __forceinline__ bool md3_own(const PhaseC& pc, uint32_t tid) {
     using S = SmemShape<T, NA, LOGN>;
     bool own = false;
     if constexpr (K == 0) own = tid < pc.j0;
-    if constexpr (K + 2 >= (int)S::J) {  // the ragged tail spans <= 2 column groups
+    if constexpr (K == (int)S::J - 1) {  // the ragged tail lies in the last column group
         const uint32_t j = (uint32_t)K * S::NTH + tid;
         if constexpr (M == NA - 1)
             own = own || (j >= pc.jend_last && j != S::N - 1);
@@ -375,7 +375,7 @@ __device__ __forceinline__ void phase_c2_split(
                 constexpr int k = 2 * kp + h;
                 constexpr uint32_t col = m * S::N + k * S::NTH;
                 sts_rot<float, 4, LOGN, m, k>(pc, e[h]);
-                if constexpr (k == 0 || k + 2 >= (int)S::J) {
+                if constexpr (k == 0 || k == (int)S::J - 1) {
                     if (!WG_EXP_NORAGGED && md3_own<float, 4, LOGN, m, k>(pc, tid))
                         ob[col] = e[h];
                 }
@@ -423,7 +423,7 @@ __device__ __forceinline__ void phase_c2(const f2_t (&u)[4][SmemShape<float, 4, 
                 constexpr uint32_t col = m * S::N + k * S::NTH;
                 sts_rot<float, 4, LOGN, m, k>(pc, MD == 3 ? e[h] : y[h]);
                 if constexpr (MD == 3) {
-                    if constexpr (k == 0 || k + 2 >= (int)S::J) {
+                    if constexpr (k == 0 || k == (int)S::J - 1) {
                         if (!WG_EXP_NORAGGED && md3_own<float, 4, LOGN, m, k>(pc, tid))
                             ob[col] = e[h];
                     }
@@ -471,7 +471,7 @@ __device__ __forceinline__ void phase_c(const T (&u)[NA][SmemShape<T, NA, LOGN>:
             if constexpr (MD == 3) {
                 const T e = y[m] + (T)0;  // 0 + 1 * v: the pool is the bulk source
                 sts_rot<T, NA, LOGN, m, k>(pc, e);
-                if constexpr (k == 0 || k + 2 >= (int)S::J) {
+                if constexpr (k == 0 || k == (int)S::J - 1) {
                     if (md3_own<T, NA, LOGN, m, k>(pc, tid)) ob[col] = e;
                 }
             } else {
@@ -765,9 +765,9 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
     const EmitCfg ec{a.mu, a.sigma, a.out_f32, a.unit};
     const bool bulk_on = EM == EM_UNIT && op == OP_FILL && a.bulk_emit != 0;
     // bulk span alignment in elements: the ragged head (< bvec) must stay
-    // inside column group 0 and the tail (< bvec + VEC) inside the last two
+    // inside column group 0 and the tail (< bvec + VEC) inside the last one
     constexpr uint32_t kVec = 16 / (uint32_t)sizeof(T);
-    constexpr uint32_t kTailCols = S::J >= 2 ? 2 * NTH : NTH;
+    constexpr uint32_t kTailCols = NTH;  // warp-stored tail: last column group only
     uint32_t bvec = 0;
     if (bulk_on) {
         bvec = kVec;
