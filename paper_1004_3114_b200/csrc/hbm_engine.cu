@@ -836,9 +836,10 @@ __global__ void __launch_bounds__(kRunThreads, 2)
     uint32_t q = 0;  // source rows consumed by this CTA so far (stage q % S)
     unsigned long long epoch = 0;  // grid barrier target
     // Emission of a freshly regenerated pool (wallace.cpp:206-213), streamed
-    // by all CTAs in 64 x 64 transpose tiles; it runs after the NEXT pass's
-    // row loads and scale are issued, so those overlap it (both only read
-    // the new pool).
+    // by all CTAs in 64 x 64 transpose tiles, the next tile's values loaded
+    // while the current one is stored.  Where it runs: WG_RUN_EMIT_MODE
+    // (default: right after the barrier that completes the pool).  `ctr`:
+    // tiles claimed from an atomic counter instead of blockIdx-strided.
     auto emit = [&](const T* e_pool, uint64_t e_n, uint64_t e_off, unsigned* ctr) {
         // natural index m*N + jh*C + jl is stored at m*N + jl*R + jh
         const uint32_t tiles_h = (R + kRunTile - 1) / kRunTile;
