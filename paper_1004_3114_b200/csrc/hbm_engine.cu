@@ -447,24 +447,80 @@ __global__ void __launch_bounds__(kSumCta) k_sum_segs(KernelArgs a, uint32_t buf
 
 constexpr uint32_t kWalkThreads = 256;
 constexpr uint32_t kBlockTerms = 32 * kSumChunk;
+constexpr uint32_t kMaxPre = 8;  // blocks whose terms the walk pre-stages
 
 // mode 0: drift_check (compare, adopt or flag ECORRUPT); mode 1: set tracked.
 template <typename T>
 __global__ void __launch_bounds__(kWalkThreads) k_sum_walk(KernelArgs a, uint32_t buf,
                                                            uint64_t nvals, const SumSeg* segs,
                                                            const SumSeg* blocks, uint32_t nch,
-                                                           int mode) {
+                                                           int mode, uint32_t maxpre) {
     extern __shared__ __align__(16) unsigned char wsm[];
     const uint32_t nblk = (nch + 31) / 32, nsup = (nblk + 31) / 32;
     SumSeg* sblk = reinterpret_cast<SumSeg*>(wsm);         // [nblk]
     SumSeg* ssup = sblk + nblk;                             // [nsup]
     SumSeg* schk = ssup + nsup;                             // [32]
-    double* sterm = reinterpret_cast<double*>(schk + 32);   // [32 * 128]
+    double* sterm = reinterpret_cast<double*>(schk + 32);   // [kBlockTerms]
+    double* spre = sterm + kBlockTerms;                     // [maxpre][kBlockTerms]
+    SumSeg* spchk = reinterpret_cast<SumSeg*>(spre + (size_t)maxpre * kBlockTerms);  // [maxpre][32]
     __shared__ uint32_t s_fail;
     __shared__ double s_q;
+    __shared__ uint32_t s_pre[kMaxPre], s_npre, s_wcnt[kWalkThreads / 32];
     if (a.meta->error) return;
-    const uint32_t t = threadIdx.x;
+    const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
     for (uint32_t b = t; b < nblk; b += kWalkThreads) sblk[b] = blocks[b];
+    if (t == 0) s_npre = 0;
+    __syncthreads();
+    // Pre-stage the terms of the first blocks whose function is invalid (a
+    // guessed binade changes inside them): the walk fails exactly there
+    // unless a guess was off, and one burst of loads replaces a latency-
+    // bound staging round per failure.  In block order (ballot compaction).
+    for (uint32_t base = 0; base < nblk && s_npre < maxpre; base += kWalkThreads) {
+        const uint32_t b = base + t;
+        const bool cand = b < nblk && !sblk[b].valid;
+        const uint32_t m = __ballot_sync(0xffffffffu, cand);
+        if (lane == 0) s_wcnt[warp] = __popc(m);
+        __syncthreads();
+        uint32_t off = s_npre;
+        for (uint32_t w = 0; w < warp; ++w) off += s_wcnt[w];
+        const uint32_t pos = off + __popc(m & ((1u << lane) - 1u));
+        if (cand && pos < maxpre) s_pre[pos] = b;
+        __syncthreads();
+        if (t == 0) {
+            uint32_t tot = s_npre;
+            for (uint32_t w = 0; w < kWalkThreads / 32; ++w) tot += s_wcnt[w];
+            s_npre = tot < maxpre ? tot : maxpre;
+        }
+        __syncthreads();
+    }
+    const uint32_t npre = s_npre;
+    {
+        const T* vv = static_cast<const T*>(a.buf[buf]);
+        const HbmSplit sp0 = hbm_split(a.N);
+        for (uint32_t j0 = 0; j0 < npre; j0 += 2) {  // two blocks' terms in flight
+            constexpr uint32_t kPer = kBlockTerms / kWalkThreads;
+            double tv[2][kPer];
+#pragma unroll
+            for (uint32_t h = 0; h < 2; ++h) {
+                const uint64_t lo = (uint64_t)s_pre[j0 + h < npre ? j0 + h : j0] * kBlockTerms;
+#pragma unroll
+                for (uint32_t k = 0; k < kPer; ++k) {
+                    const uint64_t i = lo + t + (uint64_t)k * kWalkThreads;
+                    tv[h][k] = j0 + h < npre && i < nvals ? pool_term(vv, i, a.N, sp0) : 0.0;
+                }
+            }
+#pragma unroll
+            for (uint32_t h = 0; h < 2; ++h)
+                if (j0 + h < npre)
+#pragma unroll
+                    for (uint32_t k = 0; k < kPer; ++k)
+                        spre[(size_t)(j0 + h) * kBlockTerms + t + k * kWalkThreads] = tv[h][k];
+        }
+        for (uint32_t i = t; i < npre * 32; i += kWalkThreads) {
+            const uint32_t c = s_pre[i / 32] * 32 + (i & 31u);
+            if (c < nch) spchk[i] = segs[c];
+        }
+    }
     __syncthreads();
     for (uint32_t u = t; u < nsup; u += kWalkThreads) {  // super-blocks of 32 blocks
         SumSeg g = sblk[u * 32];
@@ -499,18 +555,30 @@ __global__ void __launch_bounds__(kWalkThreads) k_sum_walk(KernelArgs a, uint32_
         __syncthreads();
         const uint32_t fb = s_fail;
         if (fb >= nblk) break;
-        // stage the failing block's chunk functions and terms
+        // the failing block's chunk functions and terms: pre-staged, or
+        // staged now
         const uint32_t c0 = fb * 32, cend = c0 + 32 < nch ? c0 + 32 : nch;
-        if (t < cend - c0) schk[t] = segs[c0 + t];
         const uint64_t lo = (uint64_t)c0 * kSumChunk, hi = umin64(lo + kBlockTerms, nvals);
-        for (uint64_t i = lo + t; i < hi; i += kWalkThreads) sterm[i - lo] = pool_term(v, i, a.N, sp);
-        __syncthreads();
+        uint32_t jp = npre;
+        for (uint32_t j = 0; j < npre; ++j)
+            if (s_pre[j] == fb) jp = j;
+        const SumSeg* ck = schk;
+        const double* tm = sterm;
+        if (jp < npre) {
+            ck = spchk + (size_t)jp * 32;
+            tm = spre + (size_t)jp * kBlockTerms;
+        } else {
+            if (t < cend - c0) schk[t] = segs[c0 + t];
+            for (uint64_t i = lo + t; i < hi; i += kWalkThreads)
+                sterm[i - lo] = pool_term(v, i, a.N, sp);
+            __syncthreads();
+        }
         if (t == 0) {
             double q = s_q;
             for (uint32_t c = c0; c < cend; ++c) {
-                if (seg_apply(q, schk[c - c0])) continue;
+                if (seg_apply(q, ck[c - c0])) continue;
                 const uint64_t l2 = (uint64_t)c * kSumChunk, h2 = umin64(l2 + kSumChunk, nvals);
-                for (uint64_t i = l2; i < h2; ++i) q = q + sterm[i - lo];
+                for (uint64_t i = l2; i < h2; ++i) q = q + tm[i - lo];
             }
             s_q = q;
         }
@@ -580,7 +648,14 @@ static cudaError_t exact_sum(uint32_t dtype, const KernelArgs& a, uint32_t buf, 
         (reinterpret_cast<uintptr_t>(cta_sum + ncta) + 63) & ~uintptr_t(63));
     SumSeg* blocks = segs + nch;
     const uint32_t nblk = (nch + 31) / 32, nsup = (nblk + 31) / 32;
-    const size_t wsm = (nblk + nsup + 32) * sizeof(SumSeg) + kBlockTerms * sizeof(double);
+    const size_t wbase = (nblk + nsup + 32) * sizeof(SumSeg) + kBlockTerms * sizeof(double);
+    // pre-staged blocks: as many (<= kMaxPre) as fit next to the rest
+    const size_t pre_each = kBlockTerms * sizeof(double) + 32 * sizeof(SumSeg);
+    const size_t kWalkSmemMax = 200 * 1024;
+    const uint32_t maxpre = wbase + pre_each > kWalkSmemMax
+                                ? 0u
+                                : (uint32_t)std::min<size_t>(kMaxPre, (kWalkSmemMax - wbase) / pre_each);
+    const size_t wsm = wbase + maxpre * pre_each;
     cudaFuncSetAttribute(k_sum_walk<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)wsm);
     cudaFuncSetAttribute(k_sum_walk<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -589,12 +664,14 @@ static cudaError_t exact_sum(uint32_t dtype, const KernelArgs& a, uint32_t buf, 
         k_sum_chunks<double><<<ncta, kSumCta, 0, st>>>(a, buf, nvals, pre_local, cta_sum, nch);
         k_sum_segs<double><<<ncta, kSumCta, 0, st>>>(a, buf, nvals, pre_local, cta_sum, segs,
                                                      blocks, nch);
-        k_sum_walk<double><<<1, kWalkThreads, wsm, st>>>(a, buf, nvals, segs, blocks, nch, mode);
+        k_sum_walk<double><<<1, kWalkThreads, wsm, st>>>(a, buf, nvals, segs, blocks, nch, mode,
+                                                         maxpre);
     } else {
         k_sum_chunks<float><<<ncta, kSumCta, 0, st>>>(a, buf, nvals, pre_local, cta_sum, nch);
         k_sum_segs<float><<<ncta, kSumCta, 0, st>>>(a, buf, nvals, pre_local, cta_sum, segs,
                                                     blocks, nch);
-        k_sum_walk<float><<<1, kWalkThreads, wsm, st>>>(a, buf, nvals, segs, blocks, nch, mode);
+        k_sum_walk<float><<<1, kWalkThreads, wsm, st>>>(a, buf, nvals, segs, blocks, nch, mode,
+                                                        maxpre);
     }
     return cudaGetLastError();
 }
