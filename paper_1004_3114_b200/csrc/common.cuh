@@ -436,6 +436,64 @@ __device__ __forceinline__ bool seg_apply(double& q, const SumSeg& g) {
     return true;
 }
 
+// Undo seg_finalize (increments are exact below 2^53; a larger one can only
+// make every prefix containing it fail to apply).
+__device__ __forceinline__ SumSeg seg_unfinalize(SumSeg g) {
+    g.s[0] = (long long)__longlong_as_double(g.s[0]);
+    g.s[1] = (long long)__longlong_as_double(g.s[1]);
+    return g;
+}
+
+__device__ __forceinline__ SumSeg seg_shfl_up(const SumSeg& g, uint32_t o) {
+    SumSeg r;
+    r.s[0] = __shfl_up_sync(0xffffffffu, g.s[0], o);
+    r.s[1] = __shfl_up_sync(0xffffffffu, g.s[1], o);
+    r.par[0] = __shfl_up_sync(0xffffffffu, g.par[0], o);
+    r.par[1] = __shfl_up_sync(0xffffffffu, g.par[1], o);
+    r.valid = __shfl_up_sync(0xffffffffu, g.valid, o);
+    r.e = __shfl_up_sync(0xffffffffu, g.e, o);
+    return r;
+}
+
+// Warp-cooperative walk over long runs of segments in one binade (the HBM
+// drift walk's blocks): applies the longest prefix of the (not finalized)
+// segments load(0 .. n-1) to the exact running sum q, 32 at a time — lane k
+// composes f_0 ... f_k by a shuffle scan and all lanes try their prefix on q
+// at once; the applicable prefixes form an initial run (once a segment is
+// invalid, changes binade or pushes Q past 2^53, every longer prefix fails
+// too).  Returns the number applied; q (warp-uniform) moves past them.
+// All 32 lanes call.  (Slower than one thread where the binade changes
+// every few segments: DESIGN.md §4.)
+template <typename Load>
+__device__ __forceinline__ uint32_t warp_seg_walk(double& q, uint32_t n, Load&& load) {
+    const uint32_t lane = threadIdx.x & 31u;
+    uint32_t done = 0;
+    while (done < n) {
+        const uint32_t k = done + lane;
+        SumSeg g;
+        if (k < n) {
+            g = load(k);
+        } else {
+            seg_init(g, 0);
+            g.valid = 0;
+        }
+#pragma unroll
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+            const SumSeg y = seg_shfl_up(g, o);
+            if (lane >= o) g = seg_compose(y, g);
+        }
+        seg_finalize(g);
+        double qk = q;
+        const bool ok = seg_apply(qk, g);
+        const uint32_t m = __ballot_sync(0xffffffffu, ok);
+        const uint32_t cnt = ~m == 0u ? 32u : (uint32_t)__ffs(~m) - 1u;  // leading run
+        if (cnt) q = __shfl_sync(0xffffffffu, qk, cnt - 1);
+        done += cnt;
+        if (cnt < 32) break;
+    }
+    return done < n ? done : n;
+}
+
 template <typename T>
 __device__ __forceinline__ double sq_term(T v) {
     const double d = (double)v;

@@ -448,6 +448,9 @@ __global__ void __launch_bounds__(kSumCta) k_sum_segs(KernelArgs a, uint32_t buf
 constexpr uint32_t kWalkThreads = 256;
 constexpr uint32_t kBlockTerms = 32 * kSumChunk;
 constexpr uint32_t kMaxPre = 8;  // blocks whose terms the walk pre-stages
+#ifndef WG_WARP_WALK  // 1: warp 0 applies blocks / chunks 32 at a time
+#define WG_WARP_WALK 1
+#endif
 
 // mode 0: drift_check (compare, adopt or flag ECORRUPT); mode 1: set tracked.
 template <typename T>
@@ -538,7 +541,19 @@ __global__ void __launch_bounds__(kWalkThreads) k_sum_walk(KernelArgs a, uint32_
     __syncthreads();
     uint32_t b0 = 0;  // next block to apply
     while (true) {
-        if (t == 0) {
+        if (WG_WARP_WALK) {
+            // warp 0: blocks 32 at a time (prefix compositions tried at once)
+            if (warp == 0) {
+                double q = s_q;
+                const uint32_t cnt = warp_seg_walk(q, nblk - b0, [&](uint32_t k) {
+                    return seg_unfinalize(sblk[b0 + k]);
+                });
+                if (t == 0) {
+                    s_q = q;
+                    s_fail = b0 + cnt;
+                }
+            }
+        } else if (t == 0) {
             double q = s_q;
             uint32_t b = b0;
             while (b < nblk) {
@@ -573,7 +588,27 @@ __global__ void __launch_bounds__(kWalkThreads) k_sum_walk(KernelArgs a, uint32_
                 sterm[i - lo] = pool_term(v, i, a.N, sp);
             __syncthreads();
         }
-        if (t == 0) {
+        if (WG_WARP_WALK) {
+            if (warp == 0) {  // chunks 32 at a time; a failing chunk's terms on lane 0
+                double q = s_q;
+                uint32_t c = c0;
+                while (c < cend) {
+                    const uint32_t cs = c;
+                    c += warp_seg_walk(q, cend - cs, [&](uint32_t k) {
+                        return seg_unfinalize(ck[cs - c0 + k]);
+                    });
+                    if (c >= cend) break;
+                    if (lane == 0) {
+                        const uint64_t l2 = (uint64_t)c * kSumChunk,
+                                       h2 = umin64(l2 + kSumChunk, nvals);
+                        for (uint64_t i = l2; i < h2; ++i) q = q + tm[i - lo];
+                    }
+                    q = __shfl_sync(0xffffffffu, q, 0);
+                    ++c;
+                }
+                if (t == 0) s_q = q;
+            }
+        } else if (t == 0) {
             double q = s_q;
             for (uint32_t c = c0; c < cend; ++c) {
                 if (seg_apply(q, ck[c - c0])) continue;
