@@ -244,6 +244,48 @@ def test_bank_fill_c3_shape_subset(W):
     assert base == out.size
 
 
+def test_c3_full_size_segment_ends_bit_exact(W):
+    """The whole C3 step (2^34 fp32 normals, 1184 pools, ~3544 refills and
+    55 drift audits per pool, bulk-copy emission) into one device array:
+    the first and last 4096 values of several pool segments equal the
+    oracle's stream for that pool, bit for bit; the device moments of the
+    full array are within the reference's CLT-style bounds."""
+    import torch
+
+    pools = 8 * 148
+    total = 1 << 34
+    free, _ = torch.cuda.mem_get_info()
+    if free < total * 4 + (4 << 30):
+        pytest.skip("needs 64 GiB of free device memory")
+    g = gpu_state(W, pool_exponent=10, throwaway_f=1, seed=2024, n_arrays=4, dtype="f32",
+                  pools=pools, init_on_host=True)
+    out = torch.empty(total, dtype=torch.float32, device="cuda")
+    g.fill(out)
+    torch.cuda.synchronize()
+    per, extra = divmod(total, pools)
+    for p in (0, 767, 768, 1183):
+        start = p * per + min(p, extra)
+        ln = per + (1 if p < extra else 0)
+        ref = O.OracleState(pool_exponent=10, throwaway_f=1, seed=2024, stream=p, n_arrays=4,
+                            dtype=O.F32).fill(ln)
+        assert_bits(out[start:start + 4096].cpu().numpy(), ref[:4096])
+        assert_bits(out[start + ln - 4096:start + ln].cpu().numpy(), ref[-4096:])
+    # moments of all 2^34 values (fp64 sums on the device, in slabs)
+    s1 = s2 = s4 = 0.0
+    for k in range(0, total, 1 << 30):
+        x = out[k:k + (1 << 30)].double()
+        x2 = x * x
+        s1 += float(x.sum())
+        s2 += float(x2.sum())
+        s4 += float((x2 * x2).sum())
+        del x, x2
+    n = float(total)
+    m1, m2, m4 = s1 / n, s2 / n, s4 / n
+    # z-scores with variances 1, 2, 96 (stats.cpp:89-108); a generous bound
+    assert abs(m1) * n ** 0.5 < 6 and abs(m2 - 1) * (n / 2) ** 0.5 < 6 * 10
+    assert abs(m4 - 3) < 5e-3
+
+
 def test_bank_calls_continue_streams(W):
     pools = 7
     g = gpu_state(W, pool_exponent=8, throwaway_f=2, seed=9, n_arrays=4, dtype="f32", pools=pools,
