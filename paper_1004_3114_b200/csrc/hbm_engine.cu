@@ -525,7 +525,7 @@ __global__ void __launch_bounds__(kWalkThreads) k_sum_walk(KernelArgs a, uint32_
         }
     }
     __syncthreads();
-    for (uint32_t u = t; u < nsup; u += kWalkThreads) {  // super-blocks of 32 blocks
+    for (uint32_t u = t; u < (WG_WARP_WALK ? 0u : nsup); u += kWalkThreads) {  // super-blocks
         SumSeg g = sblk[u * 32];
         const uint32_t end = u * 32 + 32 < nblk ? u * 32 + 32 : nblk;
         for (uint32_t b = u * 32 + 1; b < end; ++b) g = seg_compose(g, sblk[b]);
