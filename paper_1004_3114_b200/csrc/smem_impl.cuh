@@ -317,6 +317,60 @@ __device__ __forceinline__ void phase_b2(uint32_t pool_s, uint32_t (&ixb)[4],
     });
 }
 
+#ifndef WG_GATHER_FIRST  // 1: gather all columns, then one small per-variant transform
+#define WG_GATHER_FIRST 1
+#endif
+// Variant-independent gathers of phase B (packed fp32, n = 4): u[m][kp]
+// holds the sources of columns (2kp, 2kp+1) of array m; the transform then
+// runs in place, so only ~130 instructions differ between the variants
+// (hot code shrinks by one copy of the 128 gathers).
+template <int LOGN, bool AL>
+__device__ __forceinline__ void gather_b2(uint32_t pool_s, uint32_t (&ixb)[4],
+                                          const uint32_t (&stepb)[4],
+                                          f2_t (&u)[4][SmemShape<float, 4, LOGN>::J / 2]) {
+    using S = SmemShape<float, 4, LOGN>;
+    sfor<0, (int)S::J / 2>([&](auto kc) {
+        constexpr int kp = decltype(kc)::value;
+        float g[4][2];
+        sfor<0, 2>([&](auto hc) {
+            constexpr int h = decltype(hc)::value;
+            sfor<0, 4>([&](auto mc) {
+                constexpr int m = decltype(mc)::value;
+                const uint32_t a =
+                    AL ? ((ixb[m] & S::MASKB) | pool_s) : ((ixb[m] & S::MASKB) + pool_s);
+                g[m][h] = lds<float, (uint32_t)m * S::ABYTES>(a);
+                ixb[m] += stepb[m];
+            });
+        });
+        sfor<0, 4>([&](auto mc) {
+            constexpr int m = decltype(mc)::value;
+            u[m][kp] = f2_pack(g[m][0], g[m][1]);
+        });
+    });
+}
+template <int LOGN, int VAR>
+__device__ __forceinline__ void transform_b2(f2_t (&u)[4][SmemShape<float, 4, LOGN>::J / 2]) {
+    using S = SmemShape<float, 4, LOGN>;
+    sfor<0, (int)S::J / 2>([&](auto kc) {
+        constexpr int kp = decltype(kc)::value;
+        const f2_t G0 = u[0][kp], G1 = u[1][kp], G2 = u[2][kp], G3 = u[3][kp];
+        if constexpr (VAR == 0) {
+            const f2_t PP = f2_add(G0, G1), Q = f2_sub(G0, G1);
+            const f2_t R = f2_add(G2, G3), Sd = f2_sub(G2, G3);
+            u[0][kp] = f2_add(PP, R);
+            u[1][kp] = f2_add(Q, Sd);
+            u[2][kp] = f2_sub(PP, R);
+            u[3][kp] = f2_sub(Q, Sd);
+        } else {
+            const f2_t T = f2_mul(f2_pack(0.5f, 0.5f), f2_add(f2_add(G0, G1), f2_add(G2, G3)));
+            u[0][kp] = f2_sub(T, G0);
+            u[1][kp] = f2_sub(T, G1);
+            u[2][kp] = f2_sub(T, G2);
+            u[3][kp] = f2_sub(T, G3);
+        }
+    });
+}
+
 // Store of value (m, column group k) into the rotated pool.
 template <typename T, int NA, int LOGN, int M, int K>
 __device__ __forceinline__ void sts_rot(const PhaseC& pc, T v) {
@@ -632,10 +686,17 @@ __device__ __forceinline__ bool smem_pass(uint32_t pool_s, uint32_t mode, uint32
     pc.src0 = pool_s + (pc.j0 + rot2) * ES;
     if constexpr (sizeof(T) == 4 && NA == 4 && S::J % 2 == 0) {
         f2_t u[4][S::J / 2];
-        if (variant == 0)
+        if (WG_GATHER_FIRST) {
+            gather_b2<LOGN, AL>(pool_s, ixb, stepb, u);
+            if (variant == 0)
+                transform_b2<LOGN, 0>(u);
+            else
+                transform_b2<LOGN, 1>(u);
+        } else if (variant == 0) {
             phase_b2<LOGN, 0, AL>(pool_s, ixb, stepb, u);
-        else
+        } else {
             phase_b2<LOGN, 1, AL>(pool_s, ixb, stepb, u);
+        }
         bc_barrier<EM>(bulk_on && !(kSplitC<T, NA, LOGN> && md == 3));
         phase_c2_any<LOGN, EM>(md, u, c0, pc, out_p, emit_n, ec, wh);
     } else {
