@@ -371,6 +371,46 @@ __device__ __forceinline__ void transform_b2(f2_t (&u)[4][SmemShape<float, 4, LO
     });
 }
 
+// Generic (fp64 / n = 2) counterpart: gathers into u, then the n = 4
+// transform in place (op order of phase_b).
+template <typename T, int NA, int LOGN, bool AL>
+__device__ __forceinline__ void gather_b(uint32_t pool_s, uint32_t (&ixb)[NA],
+                                         const uint32_t (&stepb)[NA],
+                                         T (&u)[NA][SmemShape<T, NA, LOGN>::J]) {
+    using S = SmemShape<T, NA, LOGN>;
+    sfor<0, (int)S::J>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        sfor<0, NA>([&](auto mc) {
+            constexpr int m = decltype(mc)::value;
+            const uint32_t a =
+                AL ? ((ixb[m] & S::MASKB) | pool_s) : ((ixb[m] & S::MASKB) + pool_s);
+            u[m][k] = lds<T, (uint32_t)m * S::ABYTES>(a);
+            ixb[m] += stepb[m];
+        });
+    });
+}
+template <typename T, int LOGN, int VAR>
+__device__ __forceinline__ void transform_b(T (&u)[4][SmemShape<T, 4, LOGN>::J]) {
+    using S = SmemShape<T, 4, LOGN>;
+    sfor<0, (int)S::J>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        const T g0 = u[0][k], g1 = u[1][k], g2 = u[2][k], g3 = u[3][k];
+        if constexpr (VAR == 0) {
+            const T pp = g0 + g1, q = g0 - g1, r = g2 + g3, s = g2 - g3;
+            u[0][k] = pp + r;
+            u[1][k] = q + s;
+            u[2][k] = pp - r;
+            u[3][k] = q - s;
+        } else {
+            const T t = (T)0.5 * ((g0 + g1) + (g2 + g3));
+            u[0][k] = t - g0;
+            u[1][k] = t - g1;
+            u[2][k] = t - g2;
+            u[3][k] = t - g3;
+        }
+    });
+}
+
 // Store of value (m, column group k) into the rotated pool.
 template <typename T, int NA, int LOGN, int M, int K>
 __device__ __forceinline__ void sts_rot(const PhaseC& pc, T v) {
@@ -701,10 +741,17 @@ __device__ __forceinline__ bool smem_pass(uint32_t pool_s, uint32_t mode, uint32
         phase_c2_any<LOGN, EM>(md, u, c0, pc, out_p, emit_n, ec, wh);
     } else {
         T u[NA][S::J];
-        if (NA == 2 || variant == 0)
+        if constexpr (NA == 4 && WG_GATHER_FIRST) {
+            gather_b<T, NA, LOGN, AL>(pool_s, ixb, stepb, u);
+            if (variant == 0)
+                transform_b<T, LOGN, 0>(u);
+            else
+                transform_b<T, LOGN, 1>(u);
+        } else if (NA == 2 || variant == 0) {
             phase_b<T, NA, LOGN, 0, AL>(pool_s, ixb, stepb, u);
-        else
+        } else {
             phase_b<T, NA, LOGN, 1, AL>(pool_s, ixb, stepb, u);
+        }
         bc_barrier<EM>(bulk_on);
         phase_c_any<T, NA, LOGN, EM>(md, u, c0, c1, pc, out_p, emit_n, ec, wh);
     }
