@@ -255,8 +255,8 @@ def test_c3_full_size_segment_ends_bit_exact(W):
     pools = 8 * 148
     total = 1 << 34
     free, _ = torch.cuda.mem_get_info()
-    if free < total * 4 + (4 << 30):
-        pytest.skip("needs 64 GiB of free device memory")
+    if free < total * 4 + (12 << 30):
+        pytest.skip("needs 76 GiB of free device memory")
     g = gpu_state(W, pool_exponent=10, throwaway_f=1, seed=2024, n_arrays=4, dtype="f32",
                   pools=pools, init_on_host=True)
     out = torch.empty(total, dtype=torch.float32, device="cuda")
@@ -272,8 +272,8 @@ def test_c3_full_size_segment_ends_bit_exact(W):
         assert_bits(out[start + ln - 4096:start + ln].cpu().numpy(), ref[-4096:])
     # moments of all 2^34 values (fp64 sums on the device, in slabs)
     s1 = s2 = s4 = 0.0
-    for k in range(0, total, 1 << 30):
-        x = out[k:k + (1 << 30)].double()
+    for k in range(0, total, 1 << 28):  # 2 GiB fp64 temporaries per slab
+        x = out[k:k + (1 << 28)].double()
         x2 = x * x
         s1 += float(x.sum())
         s2 += float(x2.sum())
