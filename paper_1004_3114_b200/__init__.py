@@ -1,7 +1,7 @@
 """B200-native Wallace normal generator (Brent's RANN4, arXiv 1004.3114).
 
 The hot path — pool regeneration passes and the exposed output stream — runs
-in hand-written sm_100a kernels (csrc/kernels.cu) behind the C ABI in
+in hand-written sm_100a kernels (csrc/*.cu, built into libwrng_gpu.so) behind the C ABI in
 include/wrng_gpu.h.  This package is the Python host mirror of the
 reference's generator interface (proj/include/wrng/wallace.hpp).
 """

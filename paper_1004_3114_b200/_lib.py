@@ -1,7 +1,7 @@
 """ctypes binding of libwrng_gpu.so (the C ABI in include/wrng_gpu.h).
 
 The product path has exactly one implementation: the sm_100a kernels in
-csrc/kernels.cu.  If the shared library is missing this module raises at
+csrc/*.cu (libwrng_gpu.so).  If the shared library is missing this module raises at
 import time — there is no CPU fallback.
 """
 from __future__ import annotations
