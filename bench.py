@@ -1,22 +1,24 @@
 #!/usr/bin/env python
 """Benchmark of the Wallace pool-regeneration hot path (BASELINE.json).
 
-Default workload:
-  N = 1 GPU : C3 — n = 4, fp32, 4 x 1024 floats per pool in shared memory,
-              8 pools per SM x 148 SMs = 1184 pools, pool c seeded
-              UniformState(2024, c), 1 pass per output, 2^34 normals per step
-              written as one contiguous fp32 array (pool-major segments).
-  N > 1     : C4 — the same pools, GPU g seeded UniformState(99 + g, c),
-              2^36 normals per step split evenly over the GPUs (strong
-              scaling), no inter-GPU communication on the generation path.
-Other configs (--config c1 | c2 | c4) print the same JSON line for those
-workloads.
+Workload at every N (one curve): C4 — n = 4, fp32,
+4 x 1024 floats per pool in shared memory, 8 pools per SM x 148 SMs = 1184
+pools per GPU, GPU g's pool c seeded UniformState(99 + g, c), 1 pass per
+output, 2^36 normals per step split evenly over the N GPUs (strong
+scaling), no inter-GPU communication on the generation path.  At N = 1
+that is C3's kernel on 4 slabs of 2^34; the N = 1 line also carries the
+exact C3 config (seed 2024, 2^34) and, measured in the same run, C1, C2 and
+the GPU at the reference's only mode (n = 2 fp64, "matched_reference").
+`--config c1 | c2 | c3` makes that config the line's workload instead.
 
-One "step" = one fill of the whole step's normals through the C ABI
-(wrng_gpu_fill_f32/_f64, device output).  `value` is device-timed whole-job
-normals/s (CUDA events on the launch stream, max over ranks).  `e2e` is the
-same metric through the same public call with a pinned HOST output buffer
-(generation overlapped with D2H inside the library), on a bounded sample.
+One "step" = the step's normals through the C ABI (wrng_gpu_fill_f32/_f64,
+device output).  `value` is device-timed whole-job normals/s (CUDA events on
+the launch stream, max over ranks).  `e2e` is the same metric through the
+same public call with a pinned HOST output buffer (generation overlapped
+with D2H inside the library), on a bounded sample.
+
+`--gpus N` without torchrun re-launches itself under torch.distributed.run
+with N ranks (one per GPU) and fails when the node has fewer GPUs.
 
 `--impl reference` times the reference's own CPU implementation (the
 unmodified library built from /root/reference into oracle/_ref) on all host
@@ -124,6 +126,32 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def free_port() -> int:
+    import socket
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    return port
+
+
+def self_launch(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: one rank per GPU, launched the
+    way the driver does it."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n:
+        print(f"bench.py: --gpus {n} needs {n} CUDA devices; this node has {have}",
+              file=sys.stderr)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -187,8 +215,8 @@ def run_reference(args, cfgname: str, world: int, rank: int):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded generator state)",
+        "higher_is_better": True, "scaling": "strong" if cfgname == "c4" else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator state)",
         "config": {"workload": c["desc"], "reference_mode": "n=2 fp64", "pool_exponent": p,
                    "throwaway_f": f, "host_threads": threads},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
@@ -232,59 +260,58 @@ def cpu_baseline_port(c, seconds_target: float):
                        f"{t:.2f} s wall")}
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
-    ap.add_argument("--total", type=int, default=None, help="override normals per step")
-    ap.add_argument("--e2e-sample", type=int, default=1 << 30)
-    ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-seconds", type=float, default=2.0)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-sample-per-thread", type=float, default=float(1 << 26))
-    args = ap.parse_args()
+def roofline_of(gen, per_gpu: int, esize: int, nslabs: int, step_ms: list, cfgname: str):
+    """Roofline of the dominant kernel: one fill kernel per output slab
+    (smem engine), or the whole step (HBM engine: persistent runs + audits);
+    algorithmic bytes = stored output bytes."""
+    peak, peak_src = peaks()
+    if gen.engine() == "smem":
+        kernel_ms = statistics.mean(step_ms) / nslabs
+        algo_bytes = per_gpu * esize / nslabs
+    else:
+        kernel_ms = statistics.mean(step_ms)
+        algo_bytes = per_gpu * esize
+    achieved = algo_bytes / (kernel_ms / 1e3) / 1e9
+    # DRAM traffic per launch: dram__bytes_read + dram__bytes_write of the
+    # committed `ncu --set full` capture (profiles/traffic.json), expressed
+    # per output byte and scaled to this launch.
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as fh:
+                tj = json.load(fh).get("c3" if cfgname == "c4" else cfgname)
+            if tj:
+                traffic = tj["dram_bytes_per_output_byte"] * algo_bytes
+                traffic_src = tj["source"]
+        except Exception:
+            traffic = None
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+            "peak_source": peak_src, "algorithmic_bytes_per_launch": algo_bytes,
+            "kernel_ms": kernel_ms}
 
-    world, rank, local = dist_setup()
-    cfgname = args.config or ("c3" if world == 1 else "c4")
-    if args.impl == "reference":
-        return run_reference(args, cfgname, world, rank)
 
-    import torch
-
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
+def make_gen(c: dict, seed: int, local: int, **over):
     from paper_1004_3114_b200 import WallaceConfig, WallaceState
 
-    from paper_1004_3114_b200.sharding import shard
+    kw = dict(pool_exponent=c["pool_exponent"], throwaway_f=c["throwaway_f"], seed=seed,
+              stream_id=0, n_arrays=c["n_arrays"], dtype=c["dtype"], pools=c["pools"],
+              device=local)
+    kw.update(over)
+    return WallaceState(WallaceConfig(**kw))
 
-    c = dict(CONFIGS[cfgname])
-    total = args.total or c["total"]
-    if cfgname == "c4":
-        # 2^36 normals in total split evenly; GPU g seeded 99 + g (strong scaling)
-        sh = shard(total, world, rank, c["seed"])
-        seed, per_gpu = sh.seed, sh.count
-        scaling = "strong"
-    else:
-        # c1..c3 at N > 1: every GPU runs the whole config on its own seed
-        seed = c["seed"] + (rank if world > 1 else 0)
-        per_gpu = total
-        scaling = "weak"
-    out_dtype = torch.float32 if c["dtype"] == "f32" else torch.float64
-    esize = 4 if c["dtype"] == "f32" else 8
 
-    gen = WallaceState(WallaceConfig(pool_exponent=c["pool_exponent"],
-                                     throwaway_f=c["throwaway_f"], seed=seed, stream_id=0,
-                                     n_arrays=c["n_arrays"], dtype=c["dtype"], pools=c["pools"],
-                                     device=local))
-    # Output buffer: the whole step when it fits in HBM, else slabs of <= 64 GiB
-    # re-used within the step (every value is still stored to HBM).
+def timed_device_fills(gen, per_gpu: int, dtype: str, steps: int, warmup: int, dev,
+                       barrier=None, on_start=None):
+    """`steps` timed steps of per_gpu normals into a device buffer (slabs of
+    <= 64 GiB re-used within the step when the step does not fit HBM; every
+    value is still stored).  Returns (step_ms list, elapsed_ms, launches,
+    nslabs)."""
+    import torch
+
+    out_dtype = torch.float32 if dtype == "f32" else torch.float64
+    esize = 4 if dtype == "f32" else 8
     free, _ = torch.cuda.mem_get_info(dev)
     slab = per_gpu
     while slab * esize > min(free - (8 << 30), 96 << 30):
@@ -300,32 +327,144 @@ def main():
             gen.fill(out[:n], stream=stream)
             left -= n
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize(dev)
     gen.synchronize()
-
-    # ---- timed region -----------------------------------------------------
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
-    if world > 1:
-        torch.distributed.barrier()
+    if on_start:
+        on_start()
+    if barrier:
+        barrier()
     torch.cuda.synchronize(dev)
     launches0 = gen.kernel_launches()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
     ev[0].record(stream)
-    for k in range(args.steps):
+    for k in range(steps):
         step()
         ev[k + 1].record(stream)
     torch.cuda.synchronize(dev)
     launches = gen.kernel_launches() - launches0
-    if world > 1:
-        torch.distributed.barrier()
-    clk = clocks.stop()
+    if barrier:
+        barrier()
     gen.synchronize()  # surfaces any device-raised error
-    step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(steps)]
     elapsed_ms = ev[0].elapsed_time(ev[-1])
+    del out
+    return step_ms, elapsed_ms, launches, nslabs
+
+
+def host_e2e(gen, n: int, dtype: str, steps: int):
+    """The public call with pinned HOST output: n normals per step."""
+    import torch
+
+    host = torch.empty(n, dtype=torch.float32 if dtype == "f32" else torch.float64,
+                       pin_memory=True)
+    hv = host.numpy()
+    gen.fill(hv)  # warm (allocates staging)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        gen.fill(hv)
+    dt = time.perf_counter() - t0
+    del hv, host
+    return dt
+
+
+def sub_bench(name: str, c: dict, seed: int, per_gpu: int, steps: int, warmup: int, local: int,
+              dev, e2e_n: int = 0, e2e_steps: int = 2, **over):
+    """A secondary config measured in the same run (N = 1 line)."""
+    import torch
+
+    gen = make_gen(c, seed, local, **over)
+    esize = 4 if c["dtype"] == "f32" else 8
+    step_ms, elapsed, launches, nslabs = timed_device_fills(gen, per_gpu, c["dtype"], steps,
+                                                            warmup, dev)
+    ms = elapsed / steps
+    r = roofline_of(gen, per_gpu, esize, nslabs, step_ms, name)
+    d = {"workload": c["desc"], "value": per_gpu / (ms / 1e3), "unit": UNIT,
+         "ms_per_step": ms, "steps": steps, "warmup": warmup, "normals_per_step": per_gpu,
+         "dtype": c["dtype"], "engine": gen.engine(), "gpu_launches": launches,
+         "roofline_frac": r["frac"], "achieved_gbs": r["achieved"]}
+    if e2e_n:
+        n = min(e2e_n, per_gpu)
+        dt = host_e2e(gen, n, c["dtype"], e2e_steps)
+        d["e2e"] = {"value": n * e2e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": n * esize,
+                    "sample": f"{n} normals per step into pinned host memory"}
+    del gen
+    torch.cuda.empty_cache()
+    return d
+
+
+MATCHED = dict(n_arrays=2, dtype="f64", pool_exponent=10, throwaway_f=1, pools=8 * SMS,
+               seed=2024, total=1 << 32,
+               desc="the reference's only mode: n=2 fp64 N=2^10 f=1, 1184 pools (seed 2024), "
+                    "2^32 normals per step")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=None)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
+    ap.add_argument("--total", type=int, default=None, help="override normals per step")
+    ap.add_argument("--e2e-sample", type=int, default=1 << 30)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=2.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the C1/C2/C3/matched-reference sub-results of the N = 1 line")
+    ap.add_argument("--ref-sample-per-thread", type=float, default=float(1 << 26))
+    args = ap.parse_args()
+
+    world, rank, local = dist_setup()
+    if "WORLD_SIZE" not in os.environ and (args.gpus or 1) > 1 and args.impl == "ours":
+        return self_launch(args.gpus)
+    if args.impl == "ours" and args.gpus is not None and args.gpus != world:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    cfgname = args.config or "c4"
+    if args.impl == "reference":
+        return run_reference(args, cfgname, max(world, args.gpus or 1), rank)
+
+    import torch
+
+    if torch.cuda.device_count() <= local:
+        print(f"bench.py: rank {rank} needs cuda:{local}; {torch.cuda.device_count()} visible",
+              file=sys.stderr)
+        return 2
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_1004_3114_b200.sharding import shard
+
+    c = dict(CONFIGS[cfgname])
+    total = args.total or c["total"]
+    if cfgname == "c4":
+        # 2^36 normals in total split evenly; GPU g seeded 99 + g (strong scaling)
+        sh = shard(total, world, rank, c["seed"])
+        seed, per_gpu = sh.seed, sh.count
+        scaling = "strong"
+    else:
+        # c1..c3 at N > 1: every GPU runs the whole config on its own seed
+        seed = c["seed"] + (rank if world > 1 else 0)
+        per_gpu = total
+        scaling = "weak"
+    esize = 4 if c["dtype"] == "f32" else 8
+    gen = make_gen(c, seed, local)
+
+    # ---- timed region -----------------------------------------------------
+    clocks = ClockSampler(local)
+    barrier = (lambda: torch.distributed.barrier()) if world > 1 else None
+    step_ms, elapsed_ms, launches, nslabs = timed_device_fills(
+        gen, per_gpu, c["dtype"], args.steps, args.warmup, dev, barrier=barrier,
+        on_start=lambda: (clocks.start(), time.sleep(0.3)))
+    clk = clocks.stop()
     if world > 1:
         t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -333,60 +472,25 @@ def main():
     ms_per_step = elapsed_ms / args.steps
     total_normals = total if cfgname == "c4" else per_gpu * world
     value = total_normals / (ms_per_step / 1e3)
-
-    # Roofline of the dominant kernel: one fill kernel per slab (smem engine),
-    # algorithmic bytes = stored output bytes.
-    peak, peak_src = peaks()
-    if gen.engine() == "smem":
-        launches_per_step = nslabs
-        kernel_ms = statistics.mean(step_ms) / launches_per_step
-        algo_bytes = per_gpu * esize / launches_per_step
-    else:
-        kernel_ms = statistics.mean(step_ms)
-        algo_bytes = per_gpu * esize
-    achieved = algo_bytes / (kernel_ms / 1e3) / 1e9
-    # DRAM traffic per launch: dram__bytes_read + dram__bytes_write of the
-    # committed `ncu --set full` capture (profiles/traffic.json), expressed
-    # per output byte and scaled to this launch.
-    traffic, traffic_src = None, None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            with open(tpath) as fh:
-                tj = json.load(fh).get(cfgname)
-            if tj:
-                traffic = tj["dram_bytes_per_output_byte"] * algo_bytes
-                traffic_src = tj["source"]
-        except Exception:
-            traffic = None
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": algo_bytes,
-                "kernel_ms": kernel_ms}
+    roofline = roofline_of(gen, per_gpu, esize, nslabs, step_ms, cfgname)
 
     # ---- e2e: same public call, HOST output (pinned), bounded sample -------
     # every rank runs it; at N > 1 the slowest rank's time counts
-    # per-rank pinned host buffer: 4 GiB at N = 1, 1 GiB per rank at N > 1
     n_e2e = min(args.e2e_sample if world == 1 else min(args.e2e_sample, 1 << 28), per_gpu)
-    host = torch.empty(n_e2e, dtype=out_dtype, pin_memory=True)
-    hv = host.numpy()
-    gen.fill(hv)  # warm (allocates staging)
-    t0 = time.perf_counter()
-    for _ in range(args.e2e_steps):
-        gen.fill(hv)
-    t1 = time.perf_counter()
-    e2e_local = n_e2e * args.e2e_steps / (t1 - t0)
+    dt = host_e2e(gen, n_e2e, c["dtype"], args.e2e_steps)
+    e2e_value = n_e2e * args.e2e_steps / dt
     if world > 1:
-        t = torch.tensor([t1 - t0], device=dev, dtype=torch.float64)
+        t = torch.tensor([dt], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_local = n_e2e * args.e2e_steps * world / float(t.item())
-    e2e = {"value": e2e_local, "unit": UNIT, "h2d_bytes_per_step": 0,
+        e2e_value = n_e2e * args.e2e_steps * world / float(t.item())
+    e2e = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 0,
            "d2h_bytes_per_step": n_e2e * esize,
            "sample": f"{n_e2e} normals per rank per step into pinned host memory via "
                      f"wrng_gpu_fill_{c['dtype']}(out_is_device=0); generator state is "
-                     f"device-resident, so no host->device input bytes"}
-    del host
+                     f"device-resident, so no host->device input bytes; PCIe-bound"}
+    engine = gen.engine()
+    del gen
+    torch.cuda.empty_cache()
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -397,7 +501,7 @@ def main():
                    "normals_per_gpu": per_gpu, "pools_per_gpu": c["pools"],
                    "n_arrays": c["n_arrays"], "pool_exponent": c["pool_exponent"],
                    "throwaway_f": c["throwaway_f"], "seed_base": c["seed"],
-                   "engine": gen.engine(), "output_slabs_per_step": nslabs,
+                   "engine": engine, "output_slabs_per_step": nslabs,
                    "l2": "output per step >> 126 MB L2 (no flush needed)",
                    "parallelism": f"independent pools, {world} GPU(s), no collective"},
         "per_gpu_value": value / world,
@@ -406,11 +510,24 @@ def main():
         "clocks": clk,
         "e2e": e2e,
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_extras:
+        # secondary configs, measured in the same run on the same box
+        line["c3"] = sub_bench("c3", CONFIGS["c3"], 2024, 1 << 34, 3, 2, local, dev)
+        line["c2"] = sub_bench("c2", CONFIGS["c2"], 7, 1 << 30, 3, 1, local, dev,
+                               e2e_n=1 << 27)
+        line["c1"] = sub_bench("c1", CONFIGS["c1"], 12345, 1 << 24, 3, 1, local, dev)
+        line["matched_reference"] = sub_bench(
+            "matched", MATCHED, 2024, MATCHED["total"], 3, 2, local, dev, e2e_n=1 << 28)
+        line["matched_reference"]["note"] = (
+            "GPU through the same C ABI at the reference arm's mode (n=2 fp64); its e2e "
+            "(fp64 into pinned host memory) is PCIe-bound, compare it with the --impl "
+            "reference line")
+    if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_port(c, args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
+        torch.distributed.barrier()
         torch.distributed.destroy_process_group()
     return 0
 

@@ -246,6 +246,83 @@ wrng_gpu_status wrng_gpu_method_fill(int32_t method, uint64_t seed, uint64_t str
 wrng_gpu_status wrng_gpu_lfg_words(uint64_t seed, uint64_t stream_id, uint32_t pools,
                                    uint64_t count, uint64_t* host_out, int32_t device);
 
+/* ---- the reference's free functions on host data ------------------------
+ * (proj/include/wrng/{uniform,wallace,reference,stats}.hpp).  These serve
+ * callers that drive passes on their own value-type pools and uniform
+ * states, as the reference's tests do; include/wrng_gpu/wallace.hpp wraps
+ * them under the reference's names.  Floating-point helpers live here (built
+ * with FMA contraction off) so their bits never depend on how the caller is
+ * compiled.  wrng_gpu_regenerate runs the pass on the GPU. */
+
+/* UniformState (uniform.hpp:16-40) as plain data; the drop-in's
+ * wrng::UniformState has exactly this layout. */
+typedef struct wrng_gpu_uniform {
+    uint64_t lag_table[607];
+    uint32_t cursor_r;
+    uint32_t cursor_s;
+    uint64_t seed;
+    uint64_t stream_id;
+    uint64_t draws;
+} wrng_gpu_uniform;
+
+/* Segment (wallace.hpp:70-75) */
+typedef struct wrng_gpu_segment {
+    uint32_t low;
+    uint32_t high;
+    int64_t jx;
+    int64_t jy;
+} wrng_gpu_segment;
+
+/* UniformState::UniformState(seed, stream_id) (uniform.cpp:23-32). */
+void wrng_gpu_uniform_seed(wrng_gpu_uniform* us, uint64_t seed, uint64_t stream_id);
+/* Pool::direct_sumsq's loop (wallace.cpp:13-18) continued from q: returns
+ * q + v[0]^2 + ... + v[n-1]^2 added left to right, each product rounded. */
+double wrng_gpu_sumsq_continue(double q, const double* v, uint64_t n);
+/* chi2_target (wallace.cpp:27-31). */
+double wrng_gpu_chi2_target(double r, uint32_t nu);
+/* rotation_from_t / rotation_from_uniform (wallace.cpp:33-49). */
+void wrng_gpu_rotation_from_t(double t, uint32_t region, double* c, double* s);
+void wrng_gpu_rotation_from_uniform(wrng_gpu_uniform* us, double* c, double* s);
+/* select_pass_params (wallace.cpp:51-70; n = 4: docs/n4_spec.md §2) on a
+ * host uniform state.  ECORRUPT (after the draws, with *out holding the
+ * drawn indices) when tracked_sumsq is not > 0; EINVAL for bad arguments. */
+wrng_gpu_status wrng_gpu_select_pass_params(wrng_gpu_uniform* us, uint32_t n_arrays, uint32_t N,
+                                            uint32_t scale_mode, double tracked_sumsq,
+                                            double withheld, wrng_gpu_params* out);
+/* plan_segments (wallace.cpp:72-111): *count receives the number of
+ * segments; they are written when out != NULL and cap >= *count.  EINVAL as
+ * the reference's invalid_argument (strides not coprime to N, offsets out of
+ * range). */
+wrng_gpu_status wrng_gpu_plan_segments(const wrng_gpu_params* p, uint32_t N,
+                                       wrng_gpu_segment* out, uint32_t cap, uint32_t* count);
+/* regenerate (wallace.cpp:113-137; n = 4: docs/n4_spec.md §3): one pass
+ * from host arrays src (n_arrays * N fp64, array-major) to dst, computed on
+ * GPU `device`; *withheld_out = dst's last value.  Synchronous. */
+wrng_gpu_status wrng_gpu_regenerate(const double* src, double* dst, uint32_t n_arrays, uint32_t N,
+                                    const wrng_gpu_params* p, double* withheld_out,
+                                    int32_t device);
+/* box_muller_pair / _next, polar_transform / _next (reference.cpp:9-37);
+ * wrng_gpu_normal_fill = box_muller_fill (method 0) / polar_fill (1)
+ * (reference.cpp:41-63). */
+wrng_gpu_status wrng_gpu_box_muller_pair(double u1, double u2, double* x, double* y);
+void wrng_gpu_box_muller_next(wrng_gpu_uniform* us, double* x, double* y);
+void wrng_gpu_polar_transform(double v1, double v2, double* x, double* y);
+void wrng_gpu_polar_next(wrng_gpu_uniform* us, double* x, double* y);
+void wrng_gpu_normal_fill(int32_t method, wrng_gpu_uniform* us, double* out, uint64_t n,
+                          double mu, double sigma);
+/* to_uv, chi2_bins' statistic, moments (+ m3), autocorr_at_lag on host
+ * arrays (stats.cpp:10-127), in the reference's sequential order.
+ * moments: out7 = {m1, m2, m3, m4, z1, z2, z4}. */
+void wrng_gpu_to_uv(double x, double y, double* u, double* v, int32_t* skip);
+wrng_gpu_status wrng_gpu_chi2_bins(const double* values, uint64_t n, uint32_t k, double lo,
+                                   double hi, double* statistic);
+wrng_gpu_status wrng_gpu_moments_host(const double* values, uint64_t n, double* out7);
+wrng_gpu_status wrng_gpu_autocorr_host(const double* values, uint64_t n, uint64_t lag,
+                                       double* r);
+/* sumsq_distribution_check's reduction (stats.cpp:136-145) of n recorded
+ * targets: mean_var = {sample mean, population variance (>= 0)}. */
+void wrng_gpu_target_stats(const double* s, uint64_t n, double* mean_var);
+
 #ifdef __cplusplus
 }
 #endif

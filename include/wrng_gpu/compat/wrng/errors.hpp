@@ -1,0 +1,3 @@
+// Reference include path -> B200 drop-in.
+#pragma once
+#include "../../errors.hpp"

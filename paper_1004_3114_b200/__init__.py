@@ -15,8 +15,15 @@ from .wallace import (  # noqa: F401
     ScaleMode,
     StateErrorKind,
     WallaceConfig,
+    UniformState,
     WallaceState,
     chi2_sf,
+    chi2_target,
+    plan_segments,
+    regenerate,
+    rotation_from_t,
+    rotation_from_uniform,
+    select_pass_params,
     device_autocorr,
     device_moments,
     device_uv_chi2,
@@ -29,5 +36,6 @@ __all__ = [
     "CorruptedStateError", "CudaError", "MalformedStateError", "PassParams", "Pool",
     "Rotation2", "ScaleMode", "StateErrorKind", "WallaceConfig", "WallaceState",
     "device_moments", "lfg_words", "device_uv_chi2", "device_autocorr", "chi2_sf", "validate",
-    "method_fill",
+    "method_fill", "UniformState", "chi2_target", "rotation_from_t", "rotation_from_uniform",
+    "select_pass_params", "plan_segments", "regenerate",
 ]

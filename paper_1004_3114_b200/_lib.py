@@ -96,7 +96,29 @@ EXPORTS = (
     "wrng_gpu_kernel_launches", "wrng_gpu_engine", "wrng_gpu_moments_f32",
     "wrng_gpu_moments_f64", "wrng_gpu_lfg_words", "wrng_gpu_uv_counts", "wrng_gpu_autocorr",
     "wrng_gpu_chi2_sf", "wrng_gpu_validate", "wrng_gpu_method_fill",
+    # the reference's free functions on host data (reference_api.cu)
+    "wrng_gpu_uniform_seed", "wrng_gpu_sumsq_continue", "wrng_gpu_chi2_target",
+    "wrng_gpu_rotation_from_t", "wrng_gpu_rotation_from_uniform", "wrng_gpu_select_pass_params",
+    "wrng_gpu_plan_segments", "wrng_gpu_regenerate", "wrng_gpu_box_muller_pair",
+    "wrng_gpu_box_muller_next", "wrng_gpu_polar_transform", "wrng_gpu_polar_next",
+    "wrng_gpu_normal_fill", "wrng_gpu_to_uv", "wrng_gpu_chi2_bins", "wrng_gpu_moments_host",
+    "wrng_gpu_autocorr_host", "wrng_gpu_target_stats",
 )
+
+
+class Uniform(C.Structure):  # wrng_gpu_uniform (UniformState, uniform.hpp:16-40)
+    _fields_ = [
+        ("lag_table", C.c_uint64 * 607),
+        ("cursor_r", C.c_uint32),
+        ("cursor_s", C.c_uint32),
+        ("seed", C.c_uint64),
+        ("stream_id", C.c_uint64),
+        ("draws", C.c_uint64),
+    ]
+
+
+class Segment(C.Structure):  # wrng_gpu_segment (Segment, wallace.hpp:70-75)
+    _fields_ = [("low", C.c_uint32), ("high", C.c_uint32), ("jx", C.c_int64), ("jy", C.c_int64)]
 
 
 def _load():
@@ -137,6 +159,25 @@ def _load():
         "wrng_gpu_validate": (C.c_int, [vp, u64, u32, u64, vp, vp, P(Validation)]),
         "wrng_gpu_method_fill": (C.c_int, [i32, u64, u64, u32, vp, i32, u64, dbl, dbl, i32, i32,
                                            vp]),
+        "wrng_gpu_uniform_seed": (None, [P(Uniform), u64, u64]),
+        "wrng_gpu_sumsq_continue": (dbl, [dbl, vp, u64]),
+        "wrng_gpu_chi2_target": (dbl, [dbl, u32]),
+        "wrng_gpu_rotation_from_t": (None, [dbl, u32, P(dbl), P(dbl)]),
+        "wrng_gpu_rotation_from_uniform": (None, [P(Uniform), P(dbl), P(dbl)]),
+        "wrng_gpu_select_pass_params": (C.c_int, [P(Uniform), u32, u32, u32, dbl, dbl,
+                                                  P(Params)]),
+        "wrng_gpu_plan_segments": (C.c_int, [P(Params), u32, vp, u32, P(u32)]),
+        "wrng_gpu_regenerate": (C.c_int, [vp, vp, u32, u32, P(Params), P(dbl), i32]),
+        "wrng_gpu_box_muller_pair": (C.c_int, [dbl, dbl, P(dbl), P(dbl)]),
+        "wrng_gpu_box_muller_next": (None, [P(Uniform), P(dbl), P(dbl)]),
+        "wrng_gpu_polar_transform": (None, [dbl, dbl, P(dbl), P(dbl)]),
+        "wrng_gpu_polar_next": (None, [P(Uniform), P(dbl), P(dbl)]),
+        "wrng_gpu_normal_fill": (None, [i32, P(Uniform), vp, u64, dbl, dbl]),
+        "wrng_gpu_to_uv": (None, [dbl, dbl, P(dbl), P(dbl), P(i32)]),
+        "wrng_gpu_chi2_bins": (C.c_int, [vp, u64, u32, dbl, dbl, P(dbl)]),
+        "wrng_gpu_moments_host": (C.c_int, [vp, u64, vp]),
+        "wrng_gpu_autocorr_host": (C.c_int, [vp, u64, u64, P(dbl)]),
+        "wrng_gpu_target_stats": (None, [vp, u64, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

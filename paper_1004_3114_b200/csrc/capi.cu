@@ -1,6 +1,7 @@
 // extern "C" implementation of include/wrng_gpu.h.
 //
-// Host-side control for the two engines (kernels.cu), the counter mirror,
+// Host-side control for the engines (smem_impl.cuh, hbm_engine.cu,
+// cluster_engine.cu), the counter mirror,
 // host-output staging (generation overlapped with D2H copies), the optional
 // host (glibc) initial pool, and state import/export in the reference's
 // "WRNG" v1 format (serialize.cpp:6-13) plus our v2 for n = 4 / f32 / banks.
@@ -56,9 +57,98 @@ const bool g_cluster = std::getenv("WRNG_GPU_CLUSTER") != nullptr;
 // HBM engine: consecutive passes run as one persistent launch (k_hbm_run);
 // WRNG_GPU_HBM_STEPWISE=1 launches one kernel per pass and per emission.
 const bool g_hbm_run = std::getenv("WRNG_GPU_HBM_STEPWISE") == nullptr;
+// WRNG_GPU_NO_WINDOW=1 sends small host fills through the device path too.
+const bool g_no_window = std::getenv("WRNG_GPU_NO_WINDOW") != nullptr;
 
 bool crossed(uint64_t before, uint64_t after, uint64_t period) {
     return period > 0 && after / period > before / period;  // wallace.cpp:182-184
+}
+
+// Host (glibc) uniform generator + Box-Muller, bit-identical to the
+// reference's UniformState / box_muller_next (uniform.cpp:13-45,
+// reference.cpp:9-22).  Used for the initial pool and for restarts of
+// WRNG_GPU_INIT_HOST handles, so those stay bit-exact across restarts.
+struct HostLfg {
+    uint64_t t[kTable];
+    uint32_t r = 0;
+    uint64_t draws = 0;
+    void seed(uint64_t seed, uint64_t stream) {  // uniform.cpp:23-32
+        uint64_t s = seed ^ ((stream << 32) | (stream >> 32));
+        for (uint32_t i = 0; i < kTable; ++i) {
+            s += 0x9E3779B97F4A7C15ull;
+            uint64_t z = s;
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            t[i] = z ^ (z >> 31);
+        }
+        r = 0;
+        for (uint32_t i = 0; i < kWarmup; ++i) word();
+        draws = 0;
+    }
+    void load(const LfgState& l) {
+        std::memcpy(t, l.table, sizeof(t));
+        r = l.r;
+        draws = l.draws;
+    }
+    void store(LfgState& l) const {
+        std::memcpy(l.table, t, sizeof(t));
+        l.r = r;
+        l.draws = draws;
+    }
+    uint64_t word() {  // uniform.cpp:34-40
+        uint32_t s = r + kGap;
+        if (s >= kTable) s -= kTable;
+        uint64_t w = t[r] + t[s];
+        t[r] = w;
+        if (++r == kTable) r = 0;
+        return w;
+    }
+    double uniform() {  // uniform.cpp:42-45
+        ++draws;
+        return (double)(word() >> 11) * 0x1.0p-53;
+    }
+};
+
+void host_box_muller(HostLfg& u, double& x, double& y) {  // reference.cpp:9-22
+    double u1 = u.uniform();
+    if (u1 == 0.0) u1 = 0x1.0p-53;
+    double u2 = u.uniform();
+    const double pi = 3.141592653589793;
+    double radius = std::sqrt(-2.0 * std::log(u1));
+    double angle = 2.0 * pi * u2;
+    x = radius * std::cos(angle);
+    y = radius * std::sin(angle);
+}
+
+// init_pool (wallace.cpp:158-167) of one pool into `vals` (natural order,
+// n_arrays * N elements of the pool dtype): box_muller_fill of every array
+// in order (N is even, so no partner is dropped), then withheld = the .x of
+// one more pair, tracked = direct_sumsq (sequential, wallace.cpp:13-18).
+void host_init_pool(HostLfg& u, uint64_t nvals, bool f64, char* vals, double& tracked,
+                    double& withheld) {
+    const double zero = 0.0;
+    for (uint64_t i = 0; i < nvals; i += 2) {
+        double x, y;
+        host_box_muller(u, x, y);
+        const double vx = zero + x, vy = zero + y;  // mu + sigma * z, mu = 0, sigma = 1
+        if (f64) {
+            reinterpret_cast<double*>(vals)[i] = vx;
+            reinterpret_cast<double*>(vals)[i + 1] = vy;
+        } else {
+            reinterpret_cast<float*>(vals)[i] = (float)vx;
+            reinterpret_cast<float*>(vals)[i + 1] = (float)vy;
+        }
+    }
+    double wx, wy;
+    host_box_muller(u, wx, wy);
+    double q = 0.0;
+    for (uint64_t i = 0; i < nvals; ++i) {
+        const double d = f64 ? reinterpret_cast<double*>(vals)[i]
+                             : (double)reinterpret_cast<float*>(vals)[i];
+        q = q + d * d;
+    }
+    tracked = q;
+    withheld = wx;
 }
 
 }  // namespace
@@ -90,7 +180,26 @@ struct wrng_gpu {
     float l2_hit = 0.f;
     uint64_t launches = 0;
     std::string err;
+    // Host window (single-pool smem handles): small host-output fills are
+    // served from a host copy of the exposed pool, so a caller filling a few
+    // values at a time (the reference's own usage, e.g. acceptance.cpp:
+    // 134-140) pays one device refill + one pool copy per refill, not a
+    // device round trip per call.  `gen` counts device operations that may
+    // change the pool; the window is valid while win_gen == gen.  Values the
+    // host consumed leave the device counters stale (meta_dirty) until the
+    // next device operation writes them (order_on).
+    std::vector<char> win;
+    uint64_t win_gen = ~0ull;
+    uint64_t gen = 0;
+    bool meta_dirty = false;
+    // Small host-output fills (<= kSmallBytes): one device slab and a pinned
+    // bounce buffer, one stream, one synchronisation (fill_host_small).
+    void* small_dev = nullptr;
+    void* small_host = nullptr;
+    PoolMeta* meta_host = nullptr;  // pinned mirror for collect()
 };
+
+constexpr size_t kSmallBytes = (size_t)16 << 20;
 
 namespace {
 
@@ -101,6 +210,19 @@ wrng_gpu_status fail(wrng_gpu* g, wrng_gpu_status s, const std::string& what) {
 
 wrng_gpu_status cuda_fail(wrng_gpu* g, cudaError_t e, const char* where) {
     return fail(g, WRNG_GPU_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// No C++ exception crosses the C ABI: host allocation failures map to
+// ENOMEM, anything else to ECUDA.
+template <class F>
+wrng_gpu_status guarded(wrng_gpu* g, F&& f) {
+    try {
+        return f();
+    } catch (const std::bad_alloc&) {
+        return fail(g, WRNG_GPU_ENOMEM, "host allocation failed");
+    } catch (...) {
+        return fail(g, WRNG_GPU_ECUDA, "unexpected host exception");
+    }
 }
 
 #define CK(expr)                                                   \
@@ -135,14 +257,29 @@ void permute_pool(const wrng_gpu* g, void* data, bool to_storage) {
     std::memcpy(d, tmp.data(), tmp.size());
 }
 
+// Restarts of WRNG_GPU_INIT_HOST handles run glibc's Box-Muller on the host
+// (the device libm differs from glibc by a few ulp), so the whole stream
+// stays bit-identical to the reference's (wallace.cpp:236).
+bool host_bm(const wrng_gpu* g) { return (g->cfg.flags & WRNG_GPU_INIT_HOST) != 0; }
+
 // Orders work on stream `s` after everything queued so far on the handle.
+// Every device operation goes through here: it invalidates the host window
+// and first writes counters the host window advanced.
 wrng_gpu_status order_on(wrng_gpu* g, cudaStream_t s) {
+    ++g->gen;
     if (g->last_set && g->last != s) {
         CK(cudaEventRecord(g->order_ev, g->last));
         CK(cudaStreamWaitEvent(s, g->order_ev, 0));
     }
     g->last = s;
     g->last_set = true;
+    if (g->meta_dirty) {
+        for (uint32_t p = 0; p < g->cfg.pools; ++p) {
+            const Ctr& c = g->ctr[p];
+            LAUNCH(launch_hbm_setmeta(g->meta + p, c.pc, c.avail, c.emitted, c.active, s));
+        }
+        g->meta_dirty = false;
+    }
     return WRNG_GPU_OK;
 }
 
@@ -180,15 +317,109 @@ KernelArgs pool_args(const wrng_gpu* g, uint32_t p) {
     return a;
 }
 
+// ---- host (glibc) initial pool: bit-identical to init_pool --------------
+wrng_gpu_status host_init(wrng_gpu* g) {
+    const uint32_t P = g->cfg.pools;
+    const size_t pbytes = g->nvals * g->esize;
+    std::vector<char> vals(pbytes * P);  // the whole bank: one H2D copy
+    std::vector<LfgState> lfg(P);
+    std::vector<PoolMeta> meta(P);
+    for (uint32_t p = 0; p < P; ++p) {
+        HostLfg u;
+        u.seed(g->cfg.seed, g->cfg.stream_id + p);
+        char* v = vals.data() + (size_t)p * pbytes;
+        meta[p] = PoolMeta{};
+        host_init_pool(u, g->nvals, g->cfg.dtype == WRNG_GPU_F64, v, meta[p].tracked[0],
+                       meta[p].withheld[0]);
+        permute_pool(g, v, true);
+        u.store(lfg[p]);
+    }
+    CK(cudaMemcpyAsync(g->buf[0], vals.data(), vals.size(), cudaMemcpyHostToDevice, g->stream));
+    CK(cudaMemcpyAsync(g->lfg, lfg.data(), sizeof(LfgState) * P, cudaMemcpyHostToDevice,
+                       g->stream));
+    CK(cudaMemcpyAsync(g->meta, meta.data(), sizeof(PoolMeta) * P, cudaMemcpyHostToDevice,
+                       g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    return WRNG_GPU_OK;
+}
+
+// restart (wallace.cpp:236 -> init_pool) of the listed pools on the host,
+// from each pool's current device uniform state: the pool in buffer `act`
+// is replaced, tracked/withheld[act] set, avail = 0.  `m` is the host copy
+// of the pools' meta (updated and written back); restart_pending := mark.
+struct PoolAct {
+    uint32_t p, act;
+};
+wrng_gpu_status host_restart(wrng_gpu* g, const std::vector<PoolAct>& which,
+                             std::vector<PoolMeta>& m, uint32_t mark, cudaStream_t s) {
+    CK(cudaStreamSynchronize(s));
+    const size_t pbytes = g->nvals * g->esize;
+    std::vector<char> vals(pbytes);
+    for (const PoolAct& pa : which) {
+        LfgState l;
+        CK(cudaMemcpyAsync(&l, g->lfg + pa.p, sizeof(l), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        HostLfg u;
+        u.load(l);
+        PoolMeta& mm = m[pa.p];
+        host_init_pool(u, g->nvals, g->cfg.dtype == WRNG_GPU_F64, vals.data(),
+                       mm.tracked[pa.act], mm.withheld[pa.act]);
+        permute_pool(g, vals.data(), true);
+        u.store(l);
+        mm.avail = 0;
+        mm.restart_pending = mark;
+        CK(cudaMemcpyAsync(static_cast<char*>(g->buf[pa.act]) + (size_t)pa.p * pbytes,
+                           vals.data(), pbytes, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(g->lfg + pa.p, &l, sizeof(l), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(g->meta + pa.p, &mm, sizeof(mm), cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));  // host buffers are reused
+    }
+    return WRNG_GPU_OK;
+}
+
+// After a smem launch with host_restart = 1: restart every pool that stopped
+// at a restart (restart_pending == 1) on the host; a fill (`resume_fill`)
+// then relaunches those pools from where they stopped, until none is left.
+wrng_gpu_status finish_host_restarts(wrng_gpu* g, KernelArgs a, bool resume_fill,
+                                     cudaStream_t s) {
+    const uint32_t P = g->cfg.pools;
+    std::vector<PoolMeta> m(P);
+    for (;;) {
+        CK(cudaStreamSynchronize(s));
+        CK(cudaMemcpyAsync(m.data(), g->meta, sizeof(PoolMeta) * P, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::vector<PoolAct> pend;
+        for (uint32_t p = 0; p < P; ++p)
+            if (m[p].restart_pending == 1 && !m[p].error) pend.push_back({p, m[p].active});
+        if (pend.empty()) return WRNG_GPU_OK;
+        wrng_gpu_status st = host_restart(g, pend, m, resume_fill ? 2u : 0u, s);
+        if (st) return st;
+        if (!resume_fill) return WRNG_GPU_OK;
+        a.resume = 1;
+        LAUNCH(launch_smem(g->cfg.n_arrays, g->cfg.dtype, a, s));
+    }
+}
+
 // Pulls device meta; on any device-raised error, resynchronises the counter
 // mirror from the device, clears the flags and reports the error.
 wrng_gpu_status collect(wrng_gpu* g) {
+    if (g->meta_dirty) {
+        wrng_gpu_status st = order_on(g, g->stream);
+        if (st) return st;
+    }
+    // the meta read is queued behind everything on the handle's streams and
+    // lands in a pinned mirror: one synchronisation per stream
+    const uint32_t P = g->cfg.pools;
+    if (g->last_set && g->last != g->stream) {
+        CK(cudaEventRecord(g->order_ev, g->last));
+        CK(cudaStreamWaitEvent(g->stream, g->order_ev, 0));
+    }
+    CK(cudaStreamSynchronize(g->copy_stream));
+    CK(cudaMemcpyAsync(g->meta_host, g->meta, sizeof(PoolMeta) * P, cudaMemcpyDeviceToHost,
+                       g->stream));
     CK(cudaStreamSynchronize(g->stream));
     if (g->last_set && g->last != g->stream) CK(cudaStreamSynchronize(g->last));
-    CK(cudaStreamSynchronize(g->copy_stream));
-    const uint32_t P = g->cfg.pools;
-    std::vector<PoolMeta> m(P);
-    CK(cudaMemcpy(m.data(), g->meta, sizeof(PoolMeta) * P, cudaMemcpyDeviceToHost));
+    std::vector<PoolMeta> m(g->meta_host, g->meta_host + P);
     uint32_t code = 0;
     for (uint32_t p = 0; p < P; ++p) {
         if (m[p].error) {
@@ -215,6 +446,17 @@ struct Ev {
     uint64_t pos = 0, take = 0, out_off = 0, emit_n = 0;
     uint32_t end_refill = 0;
 };
+
+// An audit inside a refill runs on the refill's counters (pass_count
+// advanced, avail = cap, emitted not yet counted), so a failing audit leaves
+// them where the reference's exception does (wallace.cpp:188-196).
+Ev drift_event(const Ctr& c) {
+    Ev e{Ev::DRIFT};
+    e.pos = c.pc;
+    e.take = c.avail;
+    e.out_off = c.emitted;
+    return e;
+}
 
 void plan_fill(const wrng_gpu* g, Ctr& c, uint64_t len, std::vector<Ev>* ev) {
     const uint64_t cap = g->cap, f = g->cfg.throwaway_f;
@@ -248,7 +490,7 @@ void plan_fill(const wrng_gpu* g, Ctr& c, uint64_t len, std::vector<Ev>* ev) {
             c.active ^= 1u;
         }
         c.avail = cap;
-        if (crossed(before, c.pc, D) && ev) ev->push_back(Ev{Ev::DRIFT});
+        if (crossed(before, c.pc, D) && ev) ev->push_back(drift_event(c));
         if (will_restart) {
             if (ev) ev->push_back(Ev{Ev::RESTART});
             c.avail = 0;
@@ -273,7 +515,7 @@ void plan_refill(const wrng_gpu* g, Ctr& c, std::vector<Ev>* ev) {
         c.active ^= 1u;
     }
     c.avail = g->cap;
-    if (crossed(before, c.pc, g->cfg.drift_check_period) && ev) ev->push_back(Ev{Ev::DRIFT});
+    if (crossed(before, c.pc, g->cfg.drift_check_period) && ev) ev->push_back(drift_event(c));
     if (g->cfg.restart_interval_passes > 0 &&
         crossed(before, c.pc, g->cfg.restart_interval_passes)) {
         if (ev) ev->push_back(Ev{Ev::RESTART});
@@ -297,10 +539,13 @@ wrng_gpu_status run_hbm(wrng_gpu* g, uint32_t p, Ctr c, const std::vector<Ev>& e
     const uint32_t NA = g->cfg.n_arrays, dt = g->cfg.dtype;
     size_t i = 0;
     while (i < ev.size()) {
-        // batch the parameter draws of consecutive passes (restart draws
-        // uniforms for Box-Muller and therefore splits batches)
+        // batch the parameter draws of consecutive passes up to the next
+        // audit or restart: a restart draws Box-Muller uniforms, and a
+        // failing audit must leave the uniform state where the reference's
+        // exception leaves it (no later pass drawn, wallace.cpp:188-196)
         size_t jend = i;
-        while (jend < ev.size() && ev[jend].kind != Ev::RESTART) ++jend;
+        while (jend < ev.size() && ev[jend].kind != Ev::RESTART && ev[jend].kind != Ev::DRIFT)
+            ++jend;
         uint32_t npass = 0;
         for (size_t k = i; k < jend; ++k) npass += ev[k].kind == Ev::PASS;
         if (npass) {
@@ -368,13 +613,29 @@ wrng_gpu_status run_hbm(wrng_gpu* g, uint32_t p, Ctr c, const std::vector<Ev>& e
                                         s));
             }
         }
-        if (jend < ev.size()) {  // RESTART
-            LAUNCH(launch_hbm_init(NA, dt, a, c.active, 0, g->scratch, s));
+        if (jend < ev.size() && ev[jend].kind == Ev::DRIFT) {
+            const Ev& d = ev[jend];
+            LAUNCH(launch_hbm_setmeta(a.meta, d.pos, d.take, d.out_off, c.active, s));
+            LAUNCH(launch_hbm_drift(NA, dt, a, c.active, (g->cfg.flags & WRNG_GPU_DRIFT_TREE) != 0,
+                                    g->scratch, s));
+            ++jend;
+        } else if (jend < ev.size()) {  // RESTART
+            if (host_bm(g)) {
+                std::vector<PoolMeta> m(g->cfg.pools);
+                CK(cudaStreamSynchronize(s));
+                CK(cudaMemcpyAsync(&m[p], a.meta, sizeof(PoolMeta), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                if (!m[p].error) {
+                    wrng_gpu_status st = host_restart(g, {{p, c.active}}, m, 0u, s);
+                    if (st) return st;
+                }
+            } else {
+                LAUNCH(launch_hbm_init(NA, dt, a, c.active, 0, g->scratch, s));
+            }
             ++jend;
         }
         i = jend;
     }
-    (void)p;
     return WRNG_GPU_OK;
 }
 
@@ -397,11 +658,16 @@ wrng_gpu_status fill_device(wrng_gpu* g, void* out, int out_f32, const OutLayout
         a.bulk_emit = g_bulk_emit && (reinterpret_cast<uintptr_t>(out) % (out_f32 ? 4 : 8)) == 0
                           ? g_bulk_align
                           : 0u;
+        a.host_restart = host_bm(g) && g->cfg.restart_interval_passes > 0;
         if (g_cluster && g->cfg.restart_interval_passes == 0 &&
             cluster_engine_fits(g->cfg.n_arrays, g->cfg.dtype, g->N, P))
             LAUNCH(launch_cluster(g->cfg.n_arrays, g->cfg.dtype, a, s));
         else
             LAUNCH(launch_smem(g->cfg.n_arrays, g->cfg.dtype, a, s));
+        if (a.host_restart) {
+            st = finish_host_restarts(g, a, true, s);
+            if (st) return st;
+        }
         for (uint32_t p = 0; p < P; ++p)
             plan_fill(g, g->ctr[p], lay.len_base + (p < lay.len_extra ? 1 : 0), nullptr);
         return WRNG_GPU_OK;
@@ -520,6 +786,74 @@ wrng_gpu_status fill_host(wrng_gpu* g, void* out, int out_f32, uint64_t count, d
     return collect(g);
 }
 
+wrng_gpu_status run_op(wrng_gpu* g, Op op, wrng_gpu_params* params_host);
+
+// Host-output fill of at most one refill's worth from the host window
+// (fill, wallace.cpp:198-216): refills run on the device, each exposed pool
+// is copied to the host once, and the values are emitted as mu + sigma * v
+// in fp64 (rounded once for f32 output), the device emission's arithmetic.
+wrng_gpu_status fill_window(wrng_gpu* g, void* out, int out_f32, uint64_t count, double mu,
+                            double sigma) {
+    Ctr& c = g->ctr[0];
+    const bool f64 = g->esize == 8;
+    uint64_t done = 0;
+    while (done < count) {
+        if (c.avail == 0) {
+            wrng_gpu_status st = run_op(g, OP_REFILL, nullptr);
+            if (st) return st;
+            continue;  // a restart leaves avail = 0
+        }
+        if (g->win_gen != g->gen) {
+            wrng_gpu_status st = collect(g);
+            if (st) return st;
+            g->win.resize(g->nvals * g->esize);
+            CK(cudaMemcpyAsync(g->win.data(), g->buf[c.active], g->win.size(),
+                               cudaMemcpyDeviceToHost, g->stream));
+            CK(cudaStreamSynchronize(g->stream));
+            g->win_gen = g->gen;
+        }
+        const uint64_t take = std::min(count - done, c.avail);
+        const uint64_t pos = g->cap - c.avail;
+        for (uint64_t i = 0; i < take; ++i) {
+            const double v = f64 ? reinterpret_cast<const double*>(g->win.data())[pos + i]
+                                 : (double)reinterpret_cast<const float*>(g->win.data())[pos + i];
+            const double o = mu + sigma * v;
+            if (out_f32)
+                static_cast<float*>(out)[done + i] = (float)o;
+            else
+                static_cast<double*>(out)[done + i] = o;
+        }
+        done += take;
+        c.avail -= take;
+        g->meta_dirty = true;
+    }
+    c.emitted += count;
+    g->meta_dirty = true;
+    return WRNG_GPU_OK;
+}
+
+// Host-output fill that fits kSmallBytes: generate into one device slab,
+// copy it to a pinned bounce buffer on the same stream, read the meta behind
+// it, synchronise once, then copy to the caller's (possibly pageable) memory.
+// The staged path's two slabs and copy stream only pay off for large fills.
+wrng_gpu_status fill_host_small(wrng_gpu* g, void* out, int out_f32, uint64_t count, double mu,
+                                double sigma) {
+    if (!g->small_dev) {
+        CK(cudaMalloc(&g->small_dev, kSmallBytes));
+        CK(cudaMallocHost(&g->small_host, kSmallBytes));
+    }
+    const uint32_t P = g->cfg.pools;
+    const size_t bytes = count * (out_f32 ? 4 : 8);
+    OutLayout lay{count / P, count % P, count / P, count % P};
+    wrng_gpu_status st = fill_device(g, g->small_dev, out_f32, lay, mu, sigma, g->stream);
+    if (st) return st;
+    CK(cudaMemcpyAsync(g->small_host, g->small_dev, bytes, cudaMemcpyDeviceToHost, g->stream));
+    st = collect(g);
+    if (st) return st;
+    std::memcpy(out, g->small_host, bytes);
+    return WRNG_GPU_OK;
+}
+
 wrng_gpu_status do_fill(wrng_gpu* g, void* out, int out_f32, uint64_t count, double mu,
                         double sigma, int out_is_device, void* stream) {
     if (!g) return WRNG_GPU_EINVAL;
@@ -530,6 +864,10 @@ wrng_gpu_status do_fill(wrng_gpu* g, void* out, int out_f32, uint64_t count, dou
         for (auto& c : g->ctr) plan_fill(g, c, 0, nullptr);
         return WRNG_GPU_OK;
     }
+    if (!out_is_device && g->cfg.pools == 1 && !g->hbm && count <= g->cap && !g_no_window)
+        return fill_window(g, out, out_f32, count, mu, sigma);
+    if (!out_is_device && count * (out_f32 ? 4 : 8) <= kSmallBytes && !stream)
+        return fill_host_small(g, out, out_f32, count, mu, sigma);
     if (!out_is_device)
         return fill_host(g, out, out_f32, count, mu, sigma,
                          stream ? static_cast<cudaStream_t>(stream) : g->stream);
@@ -550,12 +888,30 @@ wrng_gpu_status run_op(wrng_gpu* g, Op op, wrng_gpu_params* params_host) {
         st = ensure_params(g, P);
         if (st) return st;
     }
+    if (op == OP_RESTART && host_bm(g)) {  // restart() of a host-init handle
+        st = collect(g);
+        if (st) return st;
+        std::vector<PoolMeta> m(P);
+        CK(cudaMemcpyAsync(m.data(), g->meta, sizeof(PoolMeta) * P, cudaMemcpyDeviceToHost,
+                           g->stream));
+        std::vector<PoolAct> all;
+        for (uint32_t p = 0; p < P; ++p) all.push_back({p, g->ctr[p].active});
+        st = host_restart(g, all, m, 0u, g->stream);
+        if (st) return st;
+        for (uint32_t p = 0; p < P; ++p) g->ctr[p].avail = 0;
+        return collect(g);
+    }
     if (!g->hbm) {
         KernelArgs a = base_args(g);
         a.op = op;
         a.npasses = 1;
         a.params_out = (op == OP_PASSES && params_host) ? g->params : nullptr;
+        a.host_restart = op == OP_REFILL && host_bm(g) && g->cfg.restart_interval_passes > 0;
         LAUNCH(launch_smem(g->cfg.n_arrays, g->cfg.dtype, a, g->stream));
+        if (a.host_restart) {
+            st = finish_host_restarts(g, a, false, g->stream);
+            if (st) return st;
+        }
         for (uint32_t p = 0; p < P; ++p) {
             Ctr& c = g->ctr[p];
             if (op == OP_PASSES) {
@@ -606,93 +962,6 @@ wrng_gpu_status run_op(wrng_gpu* g, Op op, wrng_gpu_params* params_host) {
         CK(cudaMemcpy(params_host, g->params, sizeof(wrng_gpu_params) * P,
                       cudaMemcpyDeviceToHost));
     return st;
-}
-
-// ---- host (glibc) initial pool: bit-identical to init_pool --------------
-struct HostLfg {
-    uint64_t t[kTable];
-    uint32_t r = 0;
-    uint64_t draws = 0;
-    void seed(uint64_t seed, uint64_t stream) {  // uniform.cpp:23-32
-        uint64_t s = seed ^ ((stream << 32) | (stream >> 32));
-        for (uint32_t i = 0; i < kTable; ++i) {
-            s += 0x9E3779B97F4A7C15ull;
-            uint64_t z = s;
-            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-            t[i] = z ^ (z >> 31);
-        }
-        r = 0;
-        for (uint32_t i = 0; i < kWarmup; ++i) word();
-        draws = 0;
-    }
-    uint64_t word() {  // uniform.cpp:34-40
-        uint32_t s = r + kGap;
-        if (s >= kTable) s -= kTable;
-        uint64_t w = t[r] + t[s];
-        t[r] = w;
-        if (++r == kTable) r = 0;
-        return w;
-    }
-    double uniform() {  // uniform.cpp:42-45
-        ++draws;
-        return (double)(word() >> 11) * 0x1.0p-53;
-    }
-};
-
-void host_box_muller(HostLfg& u, double& x, double& y) {  // reference.cpp:9-22
-    double u1 = u.uniform();
-    if (u1 == 0.0) u1 = 0x1.0p-53;
-    double u2 = u.uniform();
-    const double pi = 3.141592653589793;
-    double radius = std::sqrt(-2.0 * std::log(u1));
-    double angle = 2.0 * pi * u2;
-    x = radius * std::cos(angle);
-    y = radius * std::sin(angle);
-}
-
-wrng_gpu_status host_init(wrng_gpu* g) {
-    const uint32_t P = g->cfg.pools;
-    std::vector<char> vals(g->nvals * g->esize);
-    std::vector<LfgState> lfg(P);
-    std::vector<PoolMeta> meta(P);
-    for (uint32_t p = 0; p < P; ++p) {
-        HostLfg u;
-        u.seed(g->cfg.seed, g->cfg.stream_id + p);
-        const double zero = 0.0;
-        for (uint64_t i = 0; i < g->nvals; i += 2) {
-            double x, y;
-            host_box_muller(u, x, y);
-            double vx = zero + x, vy = zero + y;  // mu + sigma * z, mu = 0, sigma = 1
-            if (g->cfg.dtype == WRNG_GPU_F64) {
-                reinterpret_cast<double*>(vals.data())[i] = vx;
-                reinterpret_cast<double*>(vals.data())[i + 1] = vy;
-            } else {
-                reinterpret_cast<float*>(vals.data())[i] = (float)vx;
-                reinterpret_cast<float*>(vals.data())[i + 1] = (float)vy;
-            }
-        }
-        double wx, wy;
-        host_box_muller(u, wx, wy);
-        double q = 0.0;
-        for (uint64_t i = 0; i < g->nvals; ++i) {
-            double d = g->cfg.dtype == WRNG_GPU_F64 ? reinterpret_cast<double*>(vals.data())[i]
-                                                    : (double)reinterpret_cast<float*>(vals.data())[i];
-            q = q + d * d;
-        }
-        std::memcpy(lfg[p].table, u.t, sizeof(u.t));
-        lfg[p].r = u.r;
-        lfg[p].draws = u.draws;
-        meta[p] = PoolMeta{};
-        meta[p].tracked[0] = q;
-        meta[p].withheld[0] = wx;
-        permute_pool(g, vals.data(), true);
-        CK(cudaMemcpy(static_cast<char*>(g->buf[0]) + (size_t)p * vals.size(), vals.data(),
-                      vals.size(), cudaMemcpyHostToDevice));
-    }
-    CK(cudaMemcpy(g->lfg, lfg.data(), sizeof(LfgState) * P, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(g->meta, meta.data(), sizeof(PoolMeta) * P, cudaMemcpyHostToDevice));
-    return WRNG_GPU_OK;
 }
 
 wrng_gpu_status validate(const wrng_gpu_config* c, bool check_restart) {
@@ -746,6 +1015,7 @@ wrng_gpu_status alloc_handle(const wrng_gpu_config* cfg, wrng_gpu** out) {
         }
     }
     CK(cudaMalloc(&g->meta, sizeof(PoolMeta) * cfg->pools));
+    CK(cudaMallocHost(&g->meta_host, sizeof(PoolMeta) * cfg->pools));
     CK(cudaMemset(g->meta, 0, sizeof(PoolMeta) * cfg->pools));
     CK(cudaMalloc(&g->lfg, sizeof(LfgState) * cfg->pools));
     CK(cudaMalloc(&g->scratch, g->hbm ? hbm_drift_scratch_bytes(g->nvals) : sizeof(double) * 1024));
@@ -817,9 +1087,9 @@ struct Reader {
         std::memcpy(&d, &u, 8);
         return d;
     }
-    bool raw(void* dst, size_t k) {
+    bool raw(void* dst, size_t k) {  // dst == nullptr: skip k bytes
         if (!take(k)) return false;
-        std::memcpy(dst, p + pos, k);
+        if (dst) std::memcpy(dst, p + pos, k);
         pos += k;
         return true;
     }
@@ -845,7 +1115,7 @@ void wrng_gpu_config_default(wrng_gpu_config* c) {
     c->flags = 0;
 }
 
-wrng_gpu_status wrng_gpu_create(const wrng_gpu_config* cfg, wrng_gpu_t** out) {
+static wrng_gpu_status create_impl(const wrng_gpu_config* cfg, wrng_gpu_t** out) {
     if (!cfg || !out) return WRNG_GPU_EINVAL;
     *out = nullptr;
     wrng_gpu_status st = validate(cfg, true);
@@ -882,6 +1152,10 @@ wrng_gpu_status wrng_gpu_create(const wrng_gpu_config* cfg, wrng_gpu_t** out) {
     return WRNG_GPU_OK;
 }
 
+wrng_gpu_status wrng_gpu_create(const wrng_gpu_config* cfg, wrng_gpu_t** out) {
+    return guarded(nullptr, [&] { return create_impl(cfg, out); });
+}
+
 void wrng_gpu_destroy(wrng_gpu_t* g) {
     if (!g) return;
     {
@@ -898,6 +1172,9 @@ void wrng_gpu_destroy(wrng_gpu_t* g) {
                 if (g->copy_done[b]) cudaEventDestroy(g->copy_done[b]);
             }
             if (g->meta) cudaFree(g->meta);
+            if (g->meta_host) cudaFreeHost(g->meta_host);
+            if (g->small_dev) cudaFree(g->small_dev);
+            if (g->small_host) cudaFreeHost(g->small_host);
             if (g->lfg) cudaFree(g->lfg);
             if (g->params) cudaFree(g->params);
             if (g->scratch) cudaFree(g->scratch);
@@ -912,12 +1189,12 @@ void wrng_gpu_destroy(wrng_gpu_t* g) {
 
 wrng_gpu_status wrng_gpu_fill_f64(wrng_gpu_t* g, double* out, uint64_t count, double mu,
                                   double sigma, int out_is_device, void* stream) {
-    return do_fill(g, out, 0, count, mu, sigma, out_is_device, stream);
+    return guarded(g, [&] { return do_fill(g, out, 0, count, mu, sigma, out_is_device, stream); });
 }
 
 wrng_gpu_status wrng_gpu_fill_f32(wrng_gpu_t* g, float* out, uint64_t count, double mu,
                                   double sigma, int out_is_device, void* stream) {
-    return do_fill(g, out, 1, count, mu, sigma, out_is_device, stream);
+    return guarded(g, [&] { return do_fill(g, out, 1, count, mu, sigma, out_is_device, stream); });
 }
 
 wrng_gpu_status wrng_gpu_advance_pass(wrng_gpu_t* g, wrng_gpu_params* params) {
@@ -926,7 +1203,7 @@ wrng_gpu_status wrng_gpu_advance_pass(wrng_gpu_t* g, wrng_gpu_params* params) {
         wrng_gpu_status st = ensure_params(g, g->cfg.pools);
         if (st) return st;
     }
-    return run_op(g, OP_PASSES, params);
+    return guarded(g, [&] { return run_op(g, OP_PASSES, params); });
 }
 
 wrng_gpu_status wrng_gpu_refill(wrng_gpu_t* g) {
@@ -935,17 +1212,17 @@ wrng_gpu_status wrng_gpu_refill(wrng_gpu_t* g) {
         wrng_gpu_status st = ensure_params(g, g->cfg.throwaway_f);
         if (st) return st;
     }
-    return run_op(g, OP_REFILL, nullptr);
+    return guarded(g, [&] { return run_op(g, OP_REFILL, nullptr); });
 }
 
 wrng_gpu_status wrng_gpu_drift_check(wrng_gpu_t* g) {
     if (!g) return WRNG_GPU_EINVAL;
-    return run_op(g, OP_DRIFT, nullptr);
+    return guarded(g, [&] { return run_op(g, OP_DRIFT, nullptr); });
 }
 
 wrng_gpu_status wrng_gpu_restart(wrng_gpu_t* g) {
     if (!g) return WRNG_GPU_EINVAL;
-    return run_op(g, OP_RESTART, nullptr);
+    return guarded(g, [&] { return run_op(g, OP_RESTART, nullptr); });
 }
 
 wrng_gpu_status wrng_gpu_get_config(const wrng_gpu_t* g, wrng_gpu_config* out) {
@@ -966,7 +1243,7 @@ wrng_gpu_status wrng_gpu_get_counters(const wrng_gpu_t* g, uint32_t pool,
     return WRNG_GPU_OK;
 }
 
-wrng_gpu_status wrng_gpu_read_pool(wrng_gpu_t* g, uint32_t pool, double* values,
+static wrng_gpu_status read_pool_impl(wrng_gpu_t* g, uint32_t pool, double* values,
                                    double* tracked, double* withheld) {
     if (!g || pool >= g->cfg.pools) return WRNG_GPU_EINVAL;
     DeviceGuard dg(g->cfg.device);
@@ -989,12 +1266,18 @@ wrng_gpu_status wrng_gpu_read_pool(wrng_gpu_t* g, uint32_t pool, double* values,
     return WRNG_GPU_OK;
 }
 
-wrng_gpu_status wrng_gpu_write_pool(wrng_gpu_t* g, uint32_t pool, const double* values,
+wrng_gpu_status wrng_gpu_read_pool(wrng_gpu_t* g, uint32_t pool, double* values,
+                                   double* tracked, double* withheld) {
+    return guarded(g, [&] { return read_pool_impl(g, pool, values, tracked, withheld); });
+}
+
+static wrng_gpu_status write_pool_impl(wrng_gpu_t* g, uint32_t pool, const double* values,
                                     double tracked, double withheld) {
     if (!g || pool >= g->cfg.pools) return WRNG_GPU_EINVAL;
     DeviceGuard dg(g->cfg.device);
     wrng_gpu_status st = collect(g);
     if (st) return st;
+    ++g->gen;  // the host window is stale
     PoolMeta m;
     CK(cudaMemcpy(&m, g->meta + pool, sizeof(m), cudaMemcpyDeviceToHost));
     const uint32_t act = m.active;
@@ -1016,7 +1299,12 @@ wrng_gpu_status wrng_gpu_write_pool(wrng_gpu_t* g, uint32_t pool, const double* 
     return WRNG_GPU_OK;
 }
 
-wrng_gpu_status wrng_gpu_read_uniform(wrng_gpu_t* g, uint32_t pool, uint64_t* table607,
+wrng_gpu_status wrng_gpu_write_pool(wrng_gpu_t* g, uint32_t pool, const double* values,
+                                    double tracked, double withheld) {
+    return guarded(g, [&] { return write_pool_impl(g, pool, values, tracked, withheld); });
+}
+
+static wrng_gpu_status read_uniform_impl(wrng_gpu_t* g, uint32_t pool, uint64_t* table607,
                                       uint32_t* cursor_r, uint32_t* cursor_s,
                                       uint64_t* draws) {
     if (!g || pool >= g->cfg.pools) return WRNG_GPU_EINVAL;
@@ -1032,7 +1320,13 @@ wrng_gpu_status wrng_gpu_read_uniform(wrng_gpu_t* g, uint32_t pool, uint64_t* ta
     return WRNG_GPU_OK;
 }
 
-wrng_gpu_status wrng_gpu_export_state(wrng_gpu_t* g, uint8_t* buf, size_t cap, size_t* size) {
+wrng_gpu_status wrng_gpu_read_uniform(wrng_gpu_t* g, uint32_t pool, uint64_t* table607,
+                                      uint32_t* cursor_r, uint32_t* cursor_s,
+                                      uint64_t* draws) {
+    return guarded(g, [&] { return read_uniform_impl(g, pool, table607, cursor_r, cursor_s, draws); });
+}
+
+static wrng_gpu_status export_state_impl(wrng_gpu_t* g, uint8_t* buf, size_t cap, size_t* size) {
     if (!g || !size) return WRNG_GPU_EINVAL;
     DeviceGuard dg(g->cfg.device);
     wrng_gpu_status st = collect(g);
@@ -1093,7 +1387,11 @@ wrng_gpu_status wrng_gpu_export_state(wrng_gpu_t* g, uint8_t* buf, size_t cap, s
     return WRNG_GPU_OK;
 }
 
-wrng_gpu_status wrng_gpu_import_state(const uint8_t* bytes, size_t size, int32_t device,
+wrng_gpu_status wrng_gpu_export_state(wrng_gpu_t* g, uint8_t* buf, size_t cap, size_t* size) {
+    return guarded(g, [&] { return export_state_impl(g, buf, cap, size); });
+}
+
+static wrng_gpu_status import_state_impl(const uint8_t* bytes, size_t size, int32_t device,
                                       uint32_t flags, wrng_gpu_t** out) {
     if (!out || (!bytes && size)) return WRNG_GPU_EINVAL;
     *out = nullptr;
@@ -1109,7 +1407,7 @@ wrng_gpu_status wrng_gpu_import_state(const uint8_t* bytes, size_t size, int32_t
     wrng_gpu_config c;
     wrng_gpu_config_default(&c);
     c.device = device;
-    c.flags = flags & ~WRNG_GPU_INIT_HOST;
+    c.flags = flags;  // INIT_HOST: this handle's restarts use the host Box-Muller
     c.pool_exponent = r.u32();
     if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
     if (c.pool_exponent < 8 || c.pool_exponent > 20) return WRNG_GPU_EMALFORMED_FIELD_RANGE;
@@ -1138,50 +1436,77 @@ wrng_gpu_status wrng_gpu_import_state(const uint8_t* bytes, size_t size, int32_t
     const uint64_t nvals = (uint64_t)c.n_arrays * N;
     const size_t esz = c.dtype == WRNG_GPU_F64 ? 8 : 4;
     const uint32_t P = c.pools;
-    std::vector<Ctr> ctr(P);
-    std::vector<LfgState> lfg(P);
-    std::vector<PoolMeta> meta(P);
+    const size_t body = r.pos;
+    // Two passes over the pool records.  The first reads only counters and
+    // cursors, skipping the value bytes, so a malformed input is rejected in
+    // the reference's field order before anything is allocated (a short
+    // header must not size host buffers: the record sizes are fixed by the
+    // header, the first pass proves the input holds them all).  The second,
+    // on an input now known to be exactly P records long, copies the values.
+    std::vector<Ctr> ctr;
+    std::vector<LfgState> lfg;
+    std::vector<PoolMeta> meta;
     std::vector<uint8_t> vals[2];
-    vals[0].resize(nvals * esz * P);
-    vals[1].resize(nvals * esz * P);
-    for (uint32_t p = 0; p < P; ++p) {
-        ctr[p].pc = r.u64();
-        ctr[p].emitted = r.u64();
-        ctr[p].avail = r.u64();
-        if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
-        if (ctr[p].avail > nvals - 1) return WRNG_GPU_EMALFORMED_FIELD_RANGE;
-        uint8_t act = r.u8();
-        if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
-        if (act > 1) return WRNG_GPU_EMALFORMED_FIELD_RANGE;
-        ctr[p].active = act;
-        for (uint32_t i = 0; i < kTable; ++i) lfg[p].table[i] = r.u64();
-        uint32_t cr = r.u32(), cs = r.u32();
-        if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
-        if (cr >= kTable || cs >= kTable) return WRNG_GPU_EMALFORMED_FIELD_RANGE;
-        if ((cs + kTable - cr) % kTable != kGap) return WRNG_GPU_EMALFORMED_FIELD_RANGE;
-        lfg[p].r = cr;
-        lfg[p].draws = r.u64();
-        for (int b = 0; b < 2; ++b) {
-            uint8_t* dst = vals[b].data() + p * nvals * esz;
-            if (ver == 1) {
-                for (uint64_t i = 0; i < nvals; ++i) {
-                    double d = r.f64();
-                    std::memcpy(dst + i * 8, &d, 8);
-                }
-            } else {
-                r.raw(dst, nvals * esz);
+    for (int pass = 0; pass < 2; ++pass) {
+        const bool store = pass == 1;
+        r.pos = body;
+        r.ok = true;
+        if (store) {
+            try {
+                ctr.resize(P);
+                lfg.resize(P);
+                meta.resize(P);
+                vals[0].resize(nvals * esz * P);
+                vals[1].resize(nvals * esz * P);
+            } catch (const std::bad_alloc&) {
+                return WRNG_GPU_ENOMEM;
             }
-            meta[p].tracked[b] = r.f64();
-            meta[p].withheld[b] = r.f64();
         }
-        if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
-        meta[p].pass_count = ctr[p].pc;
-        meta[p].avail = ctr[p].avail;
-        meta[p].emitted = ctr[p].emitted;
-        meta[p].active = ctr[p].active;
-        meta[p].error = 0;
+        for (uint32_t p = 0; p < P; ++p) {
+            Ctr cc;
+            LfgState ll;
+            cc.pc = r.u64();
+            cc.emitted = r.u64();
+            cc.avail = r.u64();
+            if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
+            if (cc.avail > nvals - 1) return WRNG_GPU_EMALFORMED_FIELD_RANGE;
+            uint8_t act = r.u8();
+            if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
+            if (act > 1) return WRNG_GPU_EMALFORMED_FIELD_RANGE;
+            cc.active = act;
+            for (uint32_t i = 0; i < kTable; ++i) ll.table[i] = r.u64();
+            uint32_t cr = r.u32(), cs = r.u32();
+            if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
+            if (cr >= kTable || cs >= kTable) return WRNG_GPU_EMALFORMED_FIELD_RANGE;
+            if ((cs + kTable - cr) % kTable != kGap) return WRNG_GPU_EMALFORMED_FIELD_RANGE;
+            ll.r = cr;
+            ll.pad_ = 0;
+            ll.draws = r.u64();
+            PoolMeta mm{};
+            for (int b = 0; b < 2; ++b) {
+                uint8_t* dst = store ? vals[b].data() + (size_t)p * nvals * esz : nullptr;
+                if (ver == 1) {
+                    // v1 stores doubles; the value bytes are the LE bit patterns
+                    r.raw(dst, nvals * 8);
+                } else {
+                    r.raw(dst, nvals * esz);
+                }
+                mm.tracked[b] = r.f64();
+                mm.withheld[b] = r.f64();
+            }
+            if (!r.ok) return WRNG_GPU_EMALFORMED_TRUNCATED;
+            if (store) {
+                mm.pass_count = cc.pc;
+                mm.avail = cc.avail;
+                mm.emitted = cc.emitted;
+                mm.active = cc.active;
+                ctr[p] = cc;
+                lfg[p] = ll;
+                meta[p] = mm;
+            }
+        }
+        if (r.pos != size) return WRNG_GPU_EMALFORMED_FIELD_RANGE;  // trailing bytes
     }
-    if (r.pos != size) return WRNG_GPU_EMALFORMED_FIELD_RANGE;  // trailing bytes
     wrng_gpu* g = nullptr;
     wrng_gpu_status st = alloc_handle(&c, &g);
     if (st) {
@@ -1209,6 +1534,11 @@ wrng_gpu_status wrng_gpu_import_state(const uint8_t* bytes, size_t size, int32_t
     }
     *out = g;
     return WRNG_GPU_OK;
+}
+
+wrng_gpu_status wrng_gpu_import_state(const uint8_t* bytes, size_t size, int32_t device,
+                                      uint32_t flags, wrng_gpu_t** out) {
+    return guarded(nullptr, [&] { return import_state_impl(bytes, size, device, flags, out); });
 }
 
 wrng_gpu_status wrng_gpu_synchronize(wrng_gpu_t* g) {
@@ -1390,7 +1720,7 @@ wrng_gpu_status wrng_gpu_autocorr(const void* dev, int32_t is_f32, uint64_t n, u
     return WRNG_GPU_OK;
 }
 
-wrng_gpu_status wrng_gpu_validate(wrng_gpu_t* g, uint64_t count, uint32_t k, uint64_t lag,
+static wrng_gpu_status validate_impl(wrng_gpu_t* g, uint64_t count, uint32_t k, uint64_t lag,
                                   uint64_t* counts_u, uint64_t* counts_v,
                                   wrng_gpu_validation* out) {
     if (!g || !out || k < 2 || k > 8192) return WRNG_GPU_EINVAL;
@@ -1483,6 +1813,12 @@ wrng_gpu_status wrng_gpu_validate(wrng_gpu_t* g, uint64_t count, uint32_t k, uin
     if (counts_v) std::copy(cv.begin(), cv.end(), counts_v);
     *out = v;
     return WRNG_GPU_OK;
+}
+
+wrng_gpu_status wrng_gpu_validate(wrng_gpu_t* g, uint64_t count, uint32_t k, uint64_t lag,
+                                  uint64_t* counts_u, uint64_t* counts_v,
+                                  wrng_gpu_validation* out) {
+    return guarded(g, [&] { return validate_impl(g, count, k, lag, counts_u, counts_v, out); });
 }
 
 wrng_gpu_status wrng_gpu_method_fill(int32_t method, uint64_t seed, uint64_t stream_id,

@@ -1,5 +1,5 @@
-// Internal declarations shared by kernels.cu (device code + launchers) and
-// capi.cu (the extern "C" ABI in include/wrng_gpu.h).
+// Internal declarations shared by the kernel translation units (smem_*.cu,
+// hbm_engine.cu, cluster_engine.cu, misc.cu, baselines.cu) and capi.cu (the extern "C" ABI in include/wrng_gpu.h).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -33,6 +33,14 @@ struct PoolMeta {
     uint64_t emitted;
     uint32_t active;
     uint32_t error;  // 0, or a wrng_gpu_status raised on the device
+    // Host-side restarts (WRNG_GPU_INIT_HOST handles with restarts on): a
+    // smem fill stops at a restart refill with restart_pending = 1 and
+    // fill_done = values of the call already written; the host re-initialises
+    // the pool with glibc's Box-Muller, sets restart_pending = 2 and relaunches
+    // (KernelArgs::resume), which continues pools marked 2 from fill_done.
+    uint64_t fill_done;
+    uint32_t restart_pending;
+    uint32_t pad_;
 };
 
 enum Op : uint32_t {
@@ -80,6 +88,11 @@ struct KernelArgs {
     // engine (output must be aligned to its element size); the value is the
     // output alignment in bytes of each bulk span (0 = warp stores only)
     uint32_t bulk_emit;
+    // 1: stop at a restart instead of running the device Box-Muller (the
+    // host restarts the pool, PoolMeta::restart_pending); 1 with resume = 1:
+    // continue the pools the host restarted
+    uint32_t host_restart;
+    uint32_t resume;
 };
 
 struct EngineShape {

@@ -826,6 +826,10 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
     // A device-raised error is sticky until the host observes it: the pool
     // stays frozen at the failure point.
     if (op != OP_INIT && meta->error) return;
+    // Host-restart resume launch: only the pools the host just restarted
+    // continue (PoolMeta::restart_pending == 2), from their fill_done.
+    const bool resume = a.resume != 0 && op == OP_FILL;
+    if (resume && meta->restart_pending != 2) return;
 
     // ---- load state -------------------------------------------------------
     uint64_t pc, avail, emitted;
@@ -889,8 +893,9 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
     // ---- passes in this launch (the last one keeps its source pool as the
     // inactive buffer, as advance_pass's swap does, wallace.cpp:170-174) ---
     uint64_t total_passes = 0;
+    const uint64_t done0 = resume ? meta->fill_done : 0;
     if (op == OP_FILL) {
-        uint64_t rem = len;
+        uint64_t rem = len - umin64(len, done0);
         if (avail > 0 && rem > 0) rem -= umin64(rem, avail);
         if (a.restart == 0) {
             total_passes = (rem + CAP - 1) / CAP * f;
@@ -921,7 +926,8 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
         return static_cast<T*>(a.buf[ctl->active]) + (uint64_t)p * NVALS;
     };
 
-    uint64_t done = 0;
+    uint64_t done = done0;
+    bool pending = false;  // stopped at a restart the host performs
     if (op == OP_FILL && avail > 0 && len > 0) {
         // leftover of the live pool: flat [pos, pos + take)
         const uint64_t take = umin64(len, avail);
@@ -951,7 +957,10 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
             }
             ++pass_i;
             const bool last_launch = pass_i == total_passes;
-            const bool prefetch = !last_launch && !(lastp && will_restart);
+            // no prefetch across a restart (it draws the Box-Muller uniforms
+            // first) or an audit (a failing audit leaves the uniform state
+            // where the reference's exception leaves it, wallace.cpp:192)
+            const bool prefetch = !last_launch && !(lastp && (will_restart || will_drift));
             const uint32_t en = lastp ? emit_n : 0u;
             const bool ok =
                 last_launch
@@ -976,15 +985,19 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
             break;
         }
         if (will_restart) {
-            smem_restart<T, NA, LOGN>();
             avail = 0;
             primed = false;
+            if (a.host_restart) {  // glibc Box-Muller on the host (capi.cu)
+                pending = true;
+                break;
+            }
+            smem_restart<T, NA, LOGN>();
             continue;
         }
         done += emit_n;
         avail -= emit_n;
     }
-    if (op == OP_FILL && !err) emitted += len;
+    if (op == OP_FILL && !err && !pending) emitted += len;
     if (op == OP_PASSES) {
         for (uint32_t i = 0; i < a.npasses && !err; ++i) {
             // advance_pass (wallace.cpp:169-178)
@@ -1048,6 +1061,8 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
         meta->avail = avail;
         meta->emitted = emitted;
         meta->error = (uint32_t)err;
+        meta->restart_pending = pending ? 1u : 0u;
+        meta->fill_done = done;
     }
 }
 

@@ -89,7 +89,10 @@ class WallaceConfig:
     dtype: str = "f64"         # "f64" | "f32"
     pools: int = 1             # independent pools, pool p = stream_id + p
     device: int = 0
-    init_on_host: bool = False  # glibc Box-Muller init (bit-exact with the reference)
+    # glibc Box-Muller for the initial pool and every restart: bit-exact with
+    # the reference (default, as in the C++ drop-in); False runs it on the
+    # device (CUDA libm, within a few ulp of glibc)
+    init_on_host: bool = True
     force_hbm: bool = False     # HBM-resident engine even when smem would fit
     drift_tree: bool = False    # parallel (non-reference-order) drift sum
 
@@ -194,6 +197,106 @@ class UniformStateView:
     draws: int
 
 
+# ---- the reference's free functions (wallace.hpp:77-111, uniform.hpp) -------
+class UniformState:
+    """uniform.hpp:16-40 on the host (seeded by wrng_gpu_uniform_seed; the
+    per-word recurrence mirrors uniform.cpp:34-51)."""
+
+    def __init__(self, seed: int = 0, stream_id: int = 0):
+        self._s = L.Uniform()
+        lib.wrng_gpu_uniform_seed(C.byref(self._s), seed & (2**64 - 1), stream_id & (2**64 - 1))
+
+    @property
+    def lag_table(self) -> np.ndarray:
+        return np.ctypeslib.as_array(self._s.lag_table).copy()
+
+    cursor_r = property(lambda self: self._s.cursor_r)
+    cursor_s = property(lambda self: self._s.cursor_s)
+    draws = property(lambda self: self._s.draws)
+    seed = property(lambda self: self._s.seed)
+    stream_id = property(lambda self: self._s.stream_id)
+
+    def next_word(self) -> int:
+        s = self._s
+        w = (s.lag_table[s.cursor_r] + s.lag_table[s.cursor_s]) & (2**64 - 1)
+        s.lag_table[s.cursor_r] = w
+        s.cursor_r = 0 if s.cursor_r + 1 == 607 else s.cursor_r + 1
+        s.cursor_s = 0 if s.cursor_s + 1 == 607 else s.cursor_s + 1
+        return w
+
+    def next_uniform(self) -> float:
+        self._s.draws += 1
+        return float(self.next_word() >> 11) * 2.0 ** -53
+
+    def next_int_below(self, m: int) -> int:
+        if m < 1 or m > (1 << 20):
+            raise ValueError("next_int_below: m must be in [1, 2^20]")
+        return int(self.next_uniform() * m)
+
+
+def chi2_target(r: float, nu: int) -> float:
+    """wallace.cpp:27-31."""
+    return float(lib.wrng_gpu_chi2_target(r, nu))
+
+
+def rotation_from_t(t: float, region: int) -> Rotation2:
+    """wallace.cpp:33-42."""
+    c, s = C.c_double(), C.c_double()
+    lib.wrng_gpu_rotation_from_t(t, region, C.byref(c), C.byref(s))
+    return Rotation2(c.value, s.value)
+
+
+def rotation_from_uniform(us: UniformState) -> Rotation2:
+    """wallace.cpp:44-49."""
+    c, s = C.c_double(), C.c_double()
+    lib.wrng_gpu_rotation_from_uniform(C.byref(us._s), C.byref(c), C.byref(s))
+    return Rotation2(c.value, s.value)
+
+
+def select_pass_params(us: UniformState, pool: "Pool", mode: ScaleMode = ScaleMode.chisq):
+    """wallace.cpp:51-70 (n = 4 pools: docs/n4_spec.md §2)."""
+    p = L.Params()
+    na, n = pool.arrays.shape
+    _raise(lib.wrng_gpu_select_pass_params(C.byref(us._s), na, n, int(mode), pool.tracked_sumsq,
+                                           pool.withheld, C.byref(p)), "select_pass_params")
+    return PassParams.from_c(p, na)
+
+
+def _params_c(p: "PassParams", n_arrays: int) -> L.Params:
+    c = L.Params()
+    if n_arrays == 2:
+        c.stride[0], c.stride[1], c.offset[0], c.offset[1] = p.alpha, p.beta, p.gamma, p.delta
+    else:
+        for m in range(4):
+            c.stride[m], c.offset[m] = p.strides[m], p.offsets[m]
+        c.variant = p.variant
+    c.c, c.s, c.scale, c.target_sumsq = p.rot.c, p.rot.s, p.scale, p.target_sumsq
+    return c
+
+
+def plan_segments(params: "PassParams", n: int) -> list:
+    """wallace.cpp:72-111: [(low, high, jx, jy), ...]."""
+    c = _params_c(params, 2)
+    cnt = C.c_uint32()
+    _raise(lib.wrng_gpu_plan_segments(C.byref(c), n, None, 0, C.byref(cnt)), "plan_segments")
+    segs = (L.Segment * cnt.value)()
+    _raise(lib.wrng_gpu_plan_segments(C.byref(c), n, segs, cnt.value, C.byref(cnt)),
+           "plan_segments")
+    return [(s.low, s.high, s.jx, s.jy) for s in segs]
+
+
+def regenerate(src: "Pool", params: "PassParams", device: int = 0) -> "Pool":
+    """One pass (wallace.cpp:113-137) of a host pool, computed on the GPU."""
+    na, n = src.arrays.shape
+    a = np.ascontiguousarray(src.arrays, dtype=np.float64)
+    out = np.empty_like(a)
+    c = _params_c(params, na)
+    w = C.c_double()
+    _raise(lib.wrng_gpu_regenerate(a.ctypes.data, out.ctypes.data, na, n, C.byref(c), C.byref(w),
+                                   device), "regenerate")
+    return Pool(out, params.target_sumsq, w.value)
+
+
 def _is_device_tensor(t) -> bool:
     return hasattr(t, "data_ptr") and getattr(t, "is_cuda", False)
 
@@ -285,10 +388,11 @@ class WallaceState:
 
     @classmethod
     def load_state(cls, data: bytes, device: int = 0, *, force_hbm: bool = False,
-                   drift_tree: bool = False) -> "WallaceState":
+                   drift_tree: bool = False, init_on_host: bool = True) -> "WallaceState":
         h = C.c_void_p()
         buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
-        flags = (L.FLAG_FORCE_HBM if force_hbm else 0) | (L.FLAG_DRIFT_TREE if drift_tree else 0)
+        flags = ((L.FLAG_FORCE_HBM if force_hbm else 0) | (L.FLAG_DRIFT_TREE if drift_tree else 0)
+                 | (L.FLAG_INIT_HOST if init_on_host else 0))
         _raise(lib.wrng_gpu_import_state(buf, len(data), device, flags, C.byref(h)),
                "load_state")
         return cls(_handle=h)

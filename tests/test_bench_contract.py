@@ -53,3 +53,17 @@ def test_our_arm_line():
     assert e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == (1 << 22) * 4
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+def test_gpus_flag_fails_loudly_without_enough_devices():
+    """`bench.py --gpus N` outside torchrun launches N ranks itself; with
+    fewer devices than N it must fail, not measure one GPU (CPU here)."""
+    import torch
+
+    want = max(2, torch.cuda.device_count() + 1)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(want),
+                        "--steps", "1", "--warmup", "0"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 2
+    assert f"needs {want} CUDA devices" in r.stderr
+    assert not [l for l in r.stdout.splitlines() if l.startswith("{")]
