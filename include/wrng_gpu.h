@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define WRNG_GPU_ABI_VERSION 1
+#define WRNG_GPU_ABI_VERSION 2
 
 /* Status codes.  Map 1:1 onto the reference's exceptions:
  *   EINVAL     std::invalid_argument      (wallace.cpp:141-149, 199;
@@ -222,10 +222,27 @@ typedef struct wrng_gpu_validation {
     double u_statistic, u_p, v_statistic, v_p;  /* chi2_bins of u and v */
     uint64_t lag;
     double autocorr;                  /* r at lag */
+    /* WRNG_GPU_VALIDATE_AD: Anderson-Darling A^2 of all `n` values against
+     * N(0, 1) (simple hypothesis; device radix sort, stats_ad.cu), else NAN */
+    double ad_a2;
+    uint64_t ad_n;
 } wrng_gpu_validation;
 wrng_gpu_status wrng_gpu_validate(wrng_gpu_t* g, uint64_t count, uint32_t k, uint64_t lag,
                                   uint64_t* counts_u, uint64_t* counts_v,
                                   wrng_gpu_validation* out);
+enum { WRNG_GPU_VALIDATE_AD = 1u << 0 };
+/* wrng_gpu_validate plus the statistics selected by `what` (needs device
+ * scratch of 2 keys per value for WRNG_GPU_VALIDATE_AD: 32 GiB at 2^32
+ * fp32 values; ENOMEM when it does not fit). */
+wrng_gpu_status wrng_gpu_validate_ex(wrng_gpu_t* g, uint64_t count, uint32_t k, uint64_t lag,
+                                     uint32_t what, uint64_t* counts_u, uint64_t* counts_v,
+                                     wrng_gpu_validation* out);
+/* Anderson-Darling A^2 against N(0, 1) of a DEVICE array of n values
+ * (f32 or f64), computed on the device: radix sort of order-preserving keys,
+ * then sum_j d_j with d_j = -1 - [(2j+1) ln Phi(z_j) + (2n-2j-1) ln(1-Phi(z_j))]/n
+ * in compensated arithmetic.  Synchronous; allocates 2 keys per value. */
+wrng_gpu_status wrng_gpu_anderson_darling(const void* dev, int32_t is_f32, uint64_t n, double* a2,
+                                          int32_t device, void* stream);
 
 /* ---- Box-Muller / polar baselines (reference.cpp:9-63) --
  * The methods the paper compares Wallace against, on the

@@ -629,15 +629,70 @@ static int cmp_double(const void* a, const void* b) {
 /* A^2 = -n - (1/n) sum_{i=1..n} (2i-1) [ln Phi(z_(i)) + ln(1 - Phi(z_(n+1-i)))],
  * Phi(z) = erfc(-z/sqrt2)/2 and 1 - Phi(z) = erfc(z/sqrt2)/2 (no cancellation
  * in either tail). */
-static double ad_sorted(const double* z, size_t n) {
+/* A^2 of the simple N(0,1) hypothesis on a sorted sample (new: the reference
+ * has no AD; SURVEY.md §8(c) "parity unpinned").  The textbook form
+ *   A^2 = -n - (1/n) sum_i (2i+1) [ln Phi(z_i) + ln(1 - Phi(z_{n-1-i}))]
+ * subtracts two O(n) quantities; regrouped per sorted value j,
+ *   A^2 = sum_j d_j,  d_j = -1 - [(2j+1) ln Phi(z_j) + (2n-2j-1) ln(1-Phi(z_j))] / n,
+ * every d_j is O(1) and the sum stays accurate at n = 2^32.  Summed with
+ * Neumaier compensation over [j0, j1) (the GPU kernel, stats_ad.cu, uses the
+ * same d_j). */
+static void ad_terms(const double* z, size_t n, size_t j0, size_t j1, double* sum, double* comp) {
     const double rs2 = 0.70710678118654752440;
-    double s = 0.0;
-    for (size_t i = 0; i < n; ++i) {
-        double lo = log(0.5 * erfc(-z[i] * rs2));
-        double hi = log(0.5 * erfc(z[n - 1 - i] * rs2));
-        s += (2.0 * (double)i + 1.0) * (lo + hi);
+    const double dn = (double)n;
+    double s = 0.0, c = 0.0;
+    for (size_t j = j0; j < j1; ++j) {
+        const double lo = log(0.5 * erfc(-z[j] * rs2));
+        const double hi = log(0.5 * erfc(z[j] * rs2));
+        const double wj = 2.0 * (double)j + 1.0;
+        const double d = -1.0 - (wj * lo + (2.0 * dn - wj) * hi) / dn;
+        const double t = s + d;
+        c += fabs(s) >= fabs(d) ? (s - t) + d : (d - t) + s;
+        s = t;
     }
-    return -(double)n - s / (double)n;
+    *sum = s;
+    *comp = c;
+}
+
+static double ad_sorted(const double* z, size_t n) {
+    double s, c;
+    ad_terms(z, n, 0, n, &s, &c);
+    return s + c;
+}
+
+typedef struct {
+    const double* z;
+    size_t n, j0, j1;
+    double s, c;
+} ad_job;
+
+static void* ad_worker(void* arg) {
+    ad_job* j = (ad_job*)arg;
+    ad_terms(j->z, j->n, j->j0, j->j1, &j->s, &j->c);
+    return NULL;
+}
+
+/* A^2 of an already sorted sample on `threads` host threads (large n). */
+double or_ad_sorted_threads(const double* z, size_t n, int threads) {
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    pthread_t th[256];
+    ad_job jobs[256];
+    for (int t = 0; t < threads; ++t) {
+        jobs[t].z = z;
+        jobs[t].n = n;
+        jobs[t].j0 = n * (size_t)t / (size_t)threads;
+        jobs[t].j1 = n * (size_t)(t + 1) / (size_t)threads;
+        pthread_create(&th[t], NULL, ad_worker, &jobs[t]);
+    }
+    double s = 0.0, c = 0.0;
+    for (int t = 0; t < threads; ++t) {
+        pthread_join(th[t], NULL);
+        const double d = jobs[t].s, t2 = s + d;
+        c += (fabs(s) >= fabs(d) ? (s - t2) + d : (d - t2) + s) + jobs[t].c;
+        s = t2;
+    }
+    return s + c;
 }
 
 double or_anderson_darling_f64(const double* v, size_t n) {

@@ -132,6 +132,8 @@ void or_moments_f32(const float* v, size_t n, double* out5);
 /* A^2 of the simple hypothesis N(0,1); sorts a private copy. */
 double or_anderson_darling_f64(const double* v, size_t n);
 double or_anderson_darling_f32(const float* v, size_t n);
+/* A^2 of an already sorted sample, summed on `threads` host threads. */
+double or_ad_sorted_threads(const double* z, size_t n, int threads);
 
 /* ---- uniformity and serial-correlation checks (stats.cpp:10-38, 110-127;
  * the CLI's pairing, tools/main.cpp:160-193) ---- */

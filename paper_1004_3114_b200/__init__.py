@@ -24,6 +24,7 @@ from .wallace import (  # noqa: F401
     rotation_from_t,
     rotation_from_uniform,
     select_pass_params,
+    device_anderson_darling,
     device_autocorr,
     device_moments,
     device_uv_chi2,
@@ -36,6 +37,6 @@ __all__ = [
     "CorruptedStateError", "CudaError", "MalformedStateError", "PassParams", "Pool",
     "Rotation2", "ScaleMode", "StateErrorKind", "WallaceConfig", "WallaceState",
     "device_moments", "lfg_words", "device_uv_chi2", "device_autocorr", "chi2_sf", "validate",
-    "method_fill", "UniformState", "chi2_target", "rotation_from_t", "rotation_from_uniform",
+    "method_fill", "device_anderson_darling", "UniformState", "chi2_target", "rotation_from_t", "rotation_from_uniform",
     "select_pass_params", "plan_segments", "regenerate",
 ]

@@ -82,7 +82,11 @@ class Validation(C.Structure):  # wrng_gpu_validation
         ("v_statistic", C.c_double), ("v_p", C.c_double),
         ("lag", C.c_uint64),
         ("autocorr", C.c_double),
+        ("ad_a2", C.c_double),
+        ("ad_n", C.c_uint64),
     ]
+
+VALIDATE_AD = 1 << 0
 
 
 # Every symbol include/wrng_gpu.h declares (checked by tests/test_abi.py).
@@ -103,6 +107,7 @@ EXPORTS = (
     "wrng_gpu_box_muller_next", "wrng_gpu_polar_transform", "wrng_gpu_polar_next",
     "wrng_gpu_normal_fill", "wrng_gpu_to_uv", "wrng_gpu_chi2_bins", "wrng_gpu_moments_host",
     "wrng_gpu_autocorr_host", "wrng_gpu_target_stats",
+    "wrng_gpu_validate_ex", "wrng_gpu_anderson_darling",
 )
 
 
@@ -178,6 +183,8 @@ def _load():
         "wrng_gpu_moments_host": (C.c_int, [vp, u64, vp]),
         "wrng_gpu_autocorr_host": (C.c_int, [vp, u64, u64, P(dbl)]),
         "wrng_gpu_target_stats": (None, [vp, u64, vp]),
+        "wrng_gpu_validate_ex": (C.c_int, [vp, u64, u32, u64, u32, vp, vp, P(Validation)]),
+        "wrng_gpu_anderson_darling": (C.c_int, [vp, i32, u64, P(dbl), i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -1633,8 +1633,10 @@ struct StatBufs {
     double* acc = nullptr;            // [0..3] moment sums, [4..7] lag sums
     unsigned long long* cnt = nullptr;  // [k] u, [k] v, [1] skipped
     void* tail[2] = {nullptr, nullptr};
+    void* ad = nullptr;  // A^2 keys + sort scratch
     static constexpr uint32_t kBlocks = 148 * 4;
     ~StatBufs() {
+        cudaFree(ad);
         cudaFree(part);
         cudaFree(acc);
         cudaFree(cnt);
@@ -1643,7 +1645,7 @@ struct StatBufs {
     }
     cudaError_t init(uint32_t k, size_t tail_bytes, cudaStream_t s) {
         cudaError_t e = cudaMalloc(&part, sizeof(double) * 4 * kBlocks);
-        if (e == cudaSuccess) e = cudaMalloc(&acc, sizeof(double) * 8);
+        if (e == cudaSuccess) e = cudaMalloc(&acc, sizeof(double) * 16);
         if (e == cudaSuccess) e = cudaMalloc(&cnt, sizeof(unsigned long long) * (2 * k + 1));
         if (e == cudaSuccess && tail_bytes) e = cudaMalloc(&tail[0], tail_bytes);
         if (e == cudaSuccess && tail_bytes) e = cudaMalloc(&tail[1], tail_bytes);
@@ -1721,7 +1723,7 @@ wrng_gpu_status wrng_gpu_autocorr(const void* dev, int32_t is_f32, uint64_t n, u
 }
 
 static wrng_gpu_status validate_impl(wrng_gpu_t* g, uint64_t count, uint32_t k, uint64_t lag,
-                                  uint64_t* counts_u, uint64_t* counts_v,
+                                  uint32_t what, uint64_t* counts_u, uint64_t* counts_v,
                                   wrng_gpu_validation* out) {
     if (!g || !out || k < 2 || k > 8192) return WRNG_GPU_EINVAL;
     DeviceGuard dg(g->cfg.device);
@@ -1734,6 +1736,14 @@ static wrng_gpu_status validate_impl(wrng_gpu_t* g, uint64_t count, uint32_t k, 
     cudaStream_t s = g->stream;
     StatBufs b;
     CK(b.init(k, (size_t)P * lag * esz, s));
+    const bool want_ad = (what & WRNG_GPU_VALIDATE_AD) != 0 && count > 0;
+    if (want_ad) {
+        if (cudaMalloc(&b.ad, ad_scratch_bytes(f32, count)) != cudaSuccess) {
+            (void)cudaGetLastError();
+            return fail(g, WRNG_GPU_ENOMEM, "validate: no device memory for the A^2 sort");
+        }
+    }
+    uint64_t ad_at = 0;
     // windows of L values per pool (even: pairs never straddle windows), the
     // slab kept <= 64 MiB so the reductions re-read it from L2
     const uint64_t slab = std::min<uint64_t>(g->stage_bytes, (uint64_t)64 << 20) / esz;
@@ -1759,6 +1769,10 @@ static wrng_gpu_status validate_impl(wrng_gpu_t* g, uint64_t count, uint32_t k, 
             if (gr.np == 0 || gr.len == 0) continue;
             const char* w = static_cast<const char*>(g->stage[0]) + (size_t)gr.p0 * L * esz;
             CK(launch_moment_sums(w, f32, gr.np, L, gr.len, b.part, StatBufs::kBlocks, b.acc, s));
+            if (want_ad) {
+                CK(ad_add_values(w, f32, gr.np, L, gr.len, b.ad, ad_at, s));
+                ad_at += (uint64_t)gr.np * gr.len;
+            }
             CK(launch_uv_counts(w, f32, gr.np, L, gr.len, k, b.cnt, b.cnt + k, b.cnt + 2 * k, s));
             if (lag) {
                 const size_t to = (size_t)gr.p0 * lag * esz;
@@ -1774,9 +1788,15 @@ static wrng_gpu_status validate_impl(wrng_gpu_t* g, uint64_t count, uint32_t k, 
         have = std::min<uint64_t>(lag, have + lay.len_base);
         if (tail) break;
     }
+    double a2 = NAN;
+    if (want_ad) {
+        CK(ad_finish(f32, count, b.ad, b.acc + 8, s));
+        g->launches += 2 + 5 * (f32 ? 4 : 8);
+    }
     double acc[8];
     std::vector<unsigned long long> h(2 * k + 1);
     CK(cudaStreamSynchronize(s));
+    if (want_ad) CK(cudaMemcpy(&a2, b.acc + 8, sizeof(double), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(acc, b.acc, sizeof(acc), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(h.data(), b.cnt, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
     st = collect(g);
@@ -1809,6 +1829,8 @@ static wrng_gpu_status validate_impl(wrng_gpu_t* g, uint64_t count, uint32_t k, 
         pairs += np > lag ? np - lag : 0;
     }
     v.autocorr = lag && pairs ? autocorr_from_sums(acc, count, pairs) : NAN;
+    v.ad_a2 = a2;
+    v.ad_n = want_ad ? count : 0;
     if (counts_u) std::copy(cu.begin(), cu.end(), counts_u);
     if (counts_v) std::copy(cv.begin(), cv.end(), counts_v);
     *out = v;
@@ -1818,7 +1840,37 @@ static wrng_gpu_status validate_impl(wrng_gpu_t* g, uint64_t count, uint32_t k, 
 wrng_gpu_status wrng_gpu_validate(wrng_gpu_t* g, uint64_t count, uint32_t k, uint64_t lag,
                                   uint64_t* counts_u, uint64_t* counts_v,
                                   wrng_gpu_validation* out) {
-    return guarded(g, [&] { return validate_impl(g, count, k, lag, counts_u, counts_v, out); });
+    return guarded(g, [&] { return validate_impl(g, count, k, lag, 0, counts_u, counts_v, out); });
+}
+
+wrng_gpu_status wrng_gpu_validate_ex(wrng_gpu_t* g, uint64_t count, uint32_t k, uint64_t lag,
+                                     uint32_t what, uint64_t* counts_u, uint64_t* counts_v,
+                                     wrng_gpu_validation* out) {
+    return guarded(g, [&] {
+        return validate_impl(g, count, k, lag, what, counts_u, counts_v, out);
+    });
+}
+
+wrng_gpu_status wrng_gpu_anderson_darling(const void* dev, int32_t is_f32, uint64_t n, double* a2,
+                                          int32_t device, void* stream) {
+    if (!dev || !a2 || n == 0) return WRNG_GPU_EINVAL;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return WRNG_GPU_ENODEV;
+    DeviceGuard dg(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    void* scratch = nullptr;
+    if (cudaMalloc(&scratch, ad_scratch_bytes(is_f32 ? 1 : 0, n) + 64) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return WRNG_GPU_ENOMEM;
+    }
+    double* res = reinterpret_cast<double*>(static_cast<char*>(scratch) +
+                                            ad_scratch_bytes(is_f32 ? 1 : 0, n));
+    cudaError_t e = ad_add_values(dev, is_f32 ? 1 : 0, 1, n, n, scratch, 0, s);
+    if (e == cudaSuccess) e = ad_finish(is_f32 ? 1 : 0, n, scratch, res, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaMemcpy(a2, res, sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(scratch);
+    return e == cudaSuccess ? WRNG_GPU_OK : WRNG_GPU_ECUDA;
 }
 
 wrng_gpu_status wrng_gpu_method_fill(int32_t method, uint64_t seed, uint64_t stream_id,

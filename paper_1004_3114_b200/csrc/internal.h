@@ -201,6 +201,14 @@ cudaError_t launch_ac_tail(const void* v, const void* told, void* tnew, int is_f
                            uint64_t pitch, uint64_t len, uint64_t lag, uint64_t have,
                            cudaStream_t st);
 
+// Anderson-Darling A^2 vs N(0, 1) on the device (stats_ad.cu): scratch of
+// ad_scratch_bytes(is_f32, n); keys of the sample's windows are added with
+// ad_add_values, then ad_finish sorts them and writes A^2 to *out_dev.
+size_t ad_scratch_bytes(int is_f32, uint64_t n);
+cudaError_t ad_add_values(const void* v, int is_f32, uint32_t P, uint64_t pitch, uint64_t len,
+                          void* scratch, uint64_t at, cudaStream_t st);
+cudaError_t ad_finish(int is_f32, uint64_t n, void* scratch, double* out_dev, cudaStream_t st);
+
 // Box-Muller / polar baselines (baselines.cu).
 cudaError_t launch_method_fill(int method, int f64_math, uint64_t seed, uint64_t stream0,
                                uint32_t pools, const OutLayout& lay, double mu, double sigma,

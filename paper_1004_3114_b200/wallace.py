@@ -483,6 +483,15 @@ def _dev_args(t, stream):
         stream.cuda_stream
 
 
+def device_anderson_darling(t, stream=None) -> float:
+    """A^2 of a CUDA tensor's values against N(0, 1), on the device."""
+    ptr, f32, dev, st = _dev_args(t, stream)
+    a = C.c_double()
+    _raise(lib.wrng_gpu_anderson_darling(ptr, f32, t.numel(), C.byref(a), dev, st),
+           "anderson_darling")
+    return a.value
+
+
 def chi2_sf(statistic: float, dof: int) -> float:
     """Survival function of chi-squared(dof) (stats.cpp:40-87)."""
     return float(lib.wrng_gpu_chi2_sf(statistic, dof))
@@ -523,15 +532,19 @@ def device_autocorr(t, lag: int, stream=None) -> float:
     return r.value
 
 
-def validate(state: "WallaceState", count: int, k: int = 1000, lag: int = 1) -> dict:
+def validate(state: "WallaceState", count: int, k: int = 1000, lag: int = 1,
+             ad: bool = False) -> dict:
     """Generate `count` values of `state` (advancing it exactly like
     state.fill(count)) and check them on the device: moments with z-scores,
-    u/v chi-squared, autocorrelation at `lag`.  No values reach the host."""
+    u/v chi-squared, autocorrelation at `lag`, and with ad=True the
+    Anderson-Darling A^2 of all `count` values (device radix sort).  No
+    values reach the host."""
     v = L.Validation()
     cu = np.zeros(k, dtype=np.uint64)
     cv = np.zeros(k, dtype=np.uint64)
-    _raise(lib.wrng_gpu_validate(state._h, count, k, lag, cu.ctypes.data, cv.ctypes.data,
-                                 C.byref(v)), "validate", state._h)
+    _raise(lib.wrng_gpu_validate_ex(state._h, count, k, lag, L.VALIDATE_AD if ad else 0,
+                                    cu.ctypes.data, cv.ctypes.data, C.byref(v)),
+           "validate", state._h)
     out = {f: getattr(v, f) for f, _ in L.Validation._fields_}
     out["counts_u"], out["counts_v"] = cu, cv
     return out
