@@ -176,6 +176,12 @@ wrng_gpu_status wrng_gpu_import_state(const uint8_t* bytes, size_t size, int32_t
 wrng_gpu_status wrng_gpu_synchronize(wrng_gpu_t* g);
 /* Message of the handle's last failing call ("" when none). */
 const char* wrng_gpu_last_error(const wrng_gpu_t* g);
+/* Pools the shared-memory engine keeps resident at once on cfg->device for
+ * fills of this configuration (SMs x CTAs per SM of the fill kernel): a bank
+ * of this many pools, or a multiple, runs in whole waves.  0 when the
+ * configuration runs on the HBM engine; < 0 (a negated wrng_gpu_status) on
+ * error. */
+int64_t wrng_gpu_resident_pools(const wrng_gpu_config* cfg);
 /* Number of this library's kernels launched by the handle so far. */
 uint64_t wrng_gpu_kernel_launches(const wrng_gpu_t* g);
 /* Name of the engine the handle runs: "smem" or "hbm". */

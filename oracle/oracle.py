@@ -123,6 +123,8 @@ def oracle_lib():
         lib.or_anderson_darling_f64.argtypes = [vp, C.c_size_t]
         lib.or_ad_sorted_threads.restype = dbl
         lib.or_ad_sorted_threads.argtypes = [vp, C.c_size_t, C.c_int]
+        lib.or_ad_sorted_f32_threads.restype = dbl
+        lib.or_ad_sorted_f32_threads.argtypes = [vp, C.c_size_t, C.c_int]
         lib.or_anderson_darling_f32.restype = dbl
         lib.or_anderson_darling_f32.argtypes = [vp, C.c_size_t]
         lib.or_method_bank_fill.argtypes = [C.c_int, u64, u64, u32, u64, vp]
@@ -338,11 +340,15 @@ def anderson_darling(v: np.ndarray) -> float:
 
 
 def anderson_darling_sorted(z: np.ndarray, threads: int = 0) -> float:
-    """A^2 of an already sorted float64 sample on `threads` host threads
+    """A^2 of an already sorted float32/float64 sample on `threads` host threads
     (same d_j sum as anderson_darling; for 2^32-value samples)."""
     lib = oracle_lib()
+    th = threads or (os.cpu_count() or 1)
+    if z.dtype == np.float32:
+        z = np.ascontiguousarray(z)
+        return float(lib.or_ad_sorted_f32_threads(z.ctypes.data, z.size, th))
     z = np.ascontiguousarray(z, dtype=np.float64)
-    return float(lib.or_ad_sorted_threads(z.ctypes.data, z.size, threads or (os.cpu_count() or 1)))
+    return float(lib.or_ad_sorted_threads(z.ctypes.data, z.size, th))
 
 
 def method_bank_fill(method: str, seed: int, stream0: int, pools: int, count: int) -> np.ndarray:

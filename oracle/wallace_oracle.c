@@ -637,13 +637,15 @@ static int cmp_double(const void* a, const void* b) {
  * every d_j is O(1) and the sum stays accurate at n = 2^32.  Summed with
  * Neumaier compensation over [j0, j1) (the GPU kernel, stats_ad.cu, uses the
  * same d_j). */
-static void ad_terms(const double* z, size_t n, size_t j0, size_t j1, double* sum, double* comp) {
+static void ad_terms(const double* z, const float* zf, size_t n, size_t j0, size_t j1,
+                     double* sum, double* comp) {
     const double rs2 = 0.70710678118654752440;
     const double dn = (double)n;
     double s = 0.0, c = 0.0;
     for (size_t j = j0; j < j1; ++j) {
-        const double lo = log(0.5 * erfc(-z[j] * rs2));
-        const double hi = log(0.5 * erfc(z[j] * rs2));
+        const double x = z ? z[j] : (double)zf[j];
+        const double lo = log(0.5 * erfc(-x * rs2));
+        const double hi = log(0.5 * erfc(x * rs2));
         const double wj = 2.0 * (double)j + 1.0;
         const double d = -1.0 - (wj * lo + (2.0 * dn - wj) * hi) / dn;
         const double t = s + d;
@@ -656,30 +658,31 @@ static void ad_terms(const double* z, size_t n, size_t j0, size_t j1, double* su
 
 static double ad_sorted(const double* z, size_t n) {
     double s, c;
-    ad_terms(z, n, 0, n, &s, &c);
+    ad_terms(z, NULL, n, 0, n, &s, &c);
     return s + c;
 }
 
 typedef struct {
     const double* z;
+    const float* zf;
     size_t n, j0, j1;
     double s, c;
 } ad_job;
 
 static void* ad_worker(void* arg) {
     ad_job* j = (ad_job*)arg;
-    ad_terms(j->z, j->n, j->j0, j->j1, &j->s, &j->c);
+    ad_terms(j->z, j->zf, j->n, j->j0, j->j1, &j->s, &j->c);
     return NULL;
 }
 
-/* A^2 of an already sorted sample on `threads` host threads (large n). */
-double or_ad_sorted_threads(const double* z, size_t n, int threads) {
+static double ad_sorted_threads(const double* z, const float* zf, size_t n, int threads) {
     if (threads < 1) threads = 1;
     if (threads > 256) threads = 256;
     pthread_t th[256];
     ad_job jobs[256];
     for (int t = 0; t < threads; ++t) {
         jobs[t].z = z;
+        jobs[t].zf = zf;
         jobs[t].n = n;
         jobs[t].j0 = n * (size_t)t / (size_t)threads;
         jobs[t].j1 = n * (size_t)(t + 1) / (size_t)threads;
@@ -693,6 +696,14 @@ double or_ad_sorted_threads(const double* z, size_t n, int threads) {
         s = t2;
     }
     return s + c;
+}
+
+/* A^2 of an already sorted sample on `threads` host threads (large n). */
+double or_ad_sorted_threads(const double* z, size_t n, int threads) {
+    return ad_sorted_threads(z, NULL, n, threads);
+}
+double or_ad_sorted_f32_threads(const float* z, size_t n, int threads) {
+    return ad_sorted_threads(NULL, z, n, threads);
 }
 
 double or_anderson_darling_f64(const double* v, size_t n) {

@@ -134,6 +134,7 @@ double or_anderson_darling_f64(const double* v, size_t n);
 double or_anderson_darling_f32(const float* v, size_t n);
 /* A^2 of an already sorted sample, summed on `threads` host threads. */
 double or_ad_sorted_threads(const double* z, size_t n, int threads);
+double or_ad_sorted_f32_threads(const float* z, size_t n, int threads);
 
 /* ---- uniformity and serial-correlation checks (stats.cpp:10-38, 110-127;
  * the CLI's pairing, tools/main.cpp:160-193) ---- */

@@ -29,6 +29,7 @@ from .wallace import (  # noqa: F401
     device_moments,
     device_uv_chi2,
     lfg_words,
+    resident_pools,
     method_fill,
     validate,
 )
@@ -37,6 +38,6 @@ __all__ = [
     "CorruptedStateError", "CudaError", "MalformedStateError", "PassParams", "Pool",
     "Rotation2", "ScaleMode", "StateErrorKind", "WallaceConfig", "WallaceState",
     "device_moments", "lfg_words", "device_uv_chi2", "device_autocorr", "chi2_sf", "validate",
-    "method_fill", "device_anderson_darling", "UniformState", "chi2_target", "rotation_from_t", "rotation_from_uniform",
+    "method_fill", "device_anderson_darling", "resident_pools", "UniformState", "chi2_target", "rotation_from_t", "rotation_from_uniform",
     "select_pass_params", "plan_segments", "regenerate",
 ]

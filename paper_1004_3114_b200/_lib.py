@@ -107,7 +107,7 @@ EXPORTS = (
     "wrng_gpu_box_muller_next", "wrng_gpu_polar_transform", "wrng_gpu_polar_next",
     "wrng_gpu_normal_fill", "wrng_gpu_to_uv", "wrng_gpu_chi2_bins", "wrng_gpu_moments_host",
     "wrng_gpu_autocorr_host", "wrng_gpu_target_stats",
-    "wrng_gpu_validate_ex", "wrng_gpu_anderson_darling",
+    "wrng_gpu_validate_ex", "wrng_gpu_anderson_darling", "wrng_gpu_resident_pools",
 )
 
 
@@ -185,6 +185,7 @@ def _load():
         "wrng_gpu_target_stats": (None, [vp, u64, vp]),
         "wrng_gpu_validate_ex": (C.c_int, [vp, u64, u32, u64, u32, vp, vp, P(Validation)]),
         "wrng_gpu_anderson_darling": (C.c_int, [vp, i32, u64, P(dbl), i32, vp]),
+        "wrng_gpu_resident_pools": (C.c_int64, [P(Config)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -1551,6 +1551,29 @@ const char* wrng_gpu_last_error(const wrng_gpu_t* g) { return g ? g->err.c_str()
 
 uint64_t wrng_gpu_kernel_launches(const wrng_gpu_t* g) { return g ? g->launches : 0; }
 
+int64_t wrng_gpu_resident_pools(const wrng_gpu_config* cfg) {
+    if (!cfg || validate(cfg, false) != WRNG_GPU_OK) return -(int64_t)WRNG_GPU_EINVAL;
+    const uint32_t N = 1u << cfg->pool_exponent;
+    if ((cfg->flags & WRNG_GPU_FORCE_HBM) || !smem_engine_fits(cfg->n_arrays, cfg->dtype, N))
+        return 0;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0 || cfg->device < 0 ||
+        cfg->device >= ndev)
+        return -(int64_t)WRNG_GPU_ENODEV;
+    DeviceGuard dg(cfg->device);
+    smem_engine_probe(nullptr);
+    int per_sm = 0, sms = 0;
+    KernelArgs a{};
+    a.op = OP_QUERY;
+    a.N = N;
+    a.f = cfg->throwaway_f;
+    a.out = &per_sm;
+    if (launch_smem(cfg->n_arrays, cfg->dtype, a, nullptr) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device) != cudaSuccess)
+        return -(int64_t)WRNG_GPU_ECUDA;
+    return (int64_t)per_sm * sms;
+}
+
 const char* wrng_gpu_engine(const wrng_gpu_t* g) { return g && g->hbm ? "hbm" : "smem"; }
 
 static wrng_gpu_status moments_any(const void* dev, int is_f32, uint64_t n, double* out5,

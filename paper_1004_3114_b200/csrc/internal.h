@@ -50,6 +50,7 @@ enum Op : uint32_t {
     OP_DRIFT = 3,    // drift_check
     OP_RESTART = 4,  // restart
     OP_INIT = 5,     // seed uniform generators + init_pool
+    OP_QUERY = 6,    // no launch: CTAs per SM of the fill kernel -> *(int*)out
 };
 
 // Output placement of a bank fill: pool p writes len_p values at

@@ -72,7 +72,8 @@ cudaError_t launch_smem(uint32_t n_arrays, uint32_t dtype, const KernelArgs& a,
     const bool al = aligned_layout_ok();
     // f >= 2 on small n = 4 pools: the 64-register engine (two warps per
     // 4x1024 fp32 pool) — non-emitting passes are generation-bound
-    if (n_arrays == 4 && a.op == OP_FILL && a.f >= 2 && smem_r64_fits(dtype, a.N))
+    if (n_arrays == 4 && (a.op == OP_FILL || a.op == OP_QUERY) && a.f >= 2 &&
+        smem_r64_fits(dtype, a.N))
         return smem_dispatch_n4_r64(dtype, a, st, unit_same, al);
     if (dtype == WRNG_GPU_F64)
         return n_arrays == 2 ? smem_dispatch_f64_n2(a, st, unit_same, al)

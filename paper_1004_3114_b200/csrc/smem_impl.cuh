@@ -63,6 +63,10 @@ extern __shared__ __align__(16) unsigned char g_sm[];
 
 enum EmitMode : int { EM_UNIT = 0, EM_GENERIC = 1 };
 
+#ifndef WG_RBUDGET_MIN  // smallest per-thread register budget of a shape (A/B: 255)
+#define WG_RBUDGET_MIN 128
+#endif
+
 constexpr uint32_t pick_j(uint32_t N, uint32_t regs_per_col, uint32_t data_regs) {
     uint32_t j = data_regs / regs_per_col;
     if (j > 32) j = 32;
@@ -81,8 +85,16 @@ struct SmemShape {
     static constexpr uint32_t DREGS = WG_DATA_REGS;
     static constexpr uint32_t J = pick_j(N, NA * (uint32_t)sizeof(T) / 4, DREGS);  // columns/thread
     static constexpr uint32_t NTH = N / J;                                         // CTA size
-    // registers/thread = 65536 / (NTH * MINB): 2*DREGS
-    static constexpr uint32_t MINB = NTH >= 32768 / DREGS ? 1 : (32768 / DREGS) / NTH;
+    // CTAs per SM the register budget must allow: twice the data registers
+    // J * (regs per column), at least 128 and at most 255 per thread (C3: 32
+    // threads x 8 CTAs; a 4x256 pool holds 4x fewer values per thread and runs
+    // 16 CTAs per SM)
+    static constexpr uint32_t DATA = J * (NA * (uint32_t)sizeof(T) / 4);
+    static constexpr uint32_t RBUDGET = 2 * DATA > 255                ? 255
+                                        : 2 * DATA < WG_RBUDGET_MIN ? WG_RBUDGET_MIN
+                                                                      : 2 * DATA;
+    static constexpr uint32_t MINB_R = 65536 / (NTH * RBUDGET);
+    static constexpr uint32_t MINB = MINB_R < 1 ? 1 : MINB_R > 32 ? 32 : MINB_R;
     static constexpr uint32_t MASK = N - 1;
     static constexpr uint32_t ABYTES = N * (uint32_t)sizeof(T);  // one array
     static constexpr uint32_t MASKB = MASK * (uint32_t)sizeof(T);
@@ -1073,6 +1085,9 @@ static cudaError_t go(const KernelArgs& a, cudaStream_t st) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
     if (e != cudaSuccess) return e;
+    if (a.op == OP_QUERY)
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(static_cast<int*>(a.out), kern,
+                                                             (int)S::NTH, S::BYTES);
     kern<<<a.pools, S::NTH, S::BYTES, st>>>(a);
     return cudaGetLastError();
 }

@@ -463,6 +463,17 @@ def device_moments(t, device: int = 0, stream=None) -> dict:
     return {"n": int(out[0]), "m1": out[1], "m2": out[2], "m3": out[3], "m4": out[4]}
 
 
+def resident_pools(config: WallaceConfig) -> int:
+    """Pools the shared-memory engine keeps resident at once for fills of
+    `config` on its device (SMs x CTAs per SM); 0 for HBM-engine configs.
+    Banks of this size (or a multiple) run in whole waves."""
+    c = config.to_c()
+    r = int(lib.wrng_gpu_resident_pools(C.byref(c)))
+    if r < 0:
+        _raise(-r, "resident_pools")
+    return r
+
+
 def lfg_words(seed: int, stream_id: int, pools: int, count: int, device: int = 0) -> np.ndarray:
     """First `count` next_word() outputs of UniformState(seed, stream_id + p)."""
     out = np.empty((pools, count), dtype=np.uint64)
