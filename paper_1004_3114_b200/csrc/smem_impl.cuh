@@ -63,8 +63,9 @@ extern __shared__ __align__(16) unsigned char g_sm[];
 
 enum EmitMode : int { EM_UNIT = 0, EM_GENERIC = 1 };
 
-#ifndef WG_RBUDGET_MIN  // smallest per-thread register budget of a shape (A/B: 255)
-#define WG_RBUDGET_MIN 128
+#ifndef WG_RBUDGET_MIN  // smallest per-thread register budget of a shape (128 measured slower:
+                        // 4x256 pools 32 % vs 37.5 % fp32, 66 % vs 81 % fp64)
+#define WG_RBUDGET_MIN 255
 #endif
 
 constexpr uint32_t pick_j(uint32_t N, uint32_t regs_per_col, uint32_t data_regs) {
@@ -86,9 +87,9 @@ struct SmemShape {
     static constexpr uint32_t J = pick_j(N, NA * (uint32_t)sizeof(T) / 4, DREGS);  // columns/thread
     static constexpr uint32_t NTH = N / J;                                         // CTA size
     // CTAs per SM the register budget must allow: twice the data registers
-    // J * (regs per column), at least 128 and at most 255 per thread (C3: 32
-    // threads x 8 CTAs; a 4x256 pool holds 4x fewer values per thread and runs
-    // 16 CTAs per SM)
+    // J * (regs per column), at least WG_RBUDGET_MIN and at most 255 per
+    // thread (C3: 32 threads x 8 CTAs).  A 4x256 pool could run 16 CTAs per
+    // SM at 128 registers, but measured slower than 8 at 255.
     static constexpr uint32_t DATA = J * (NA * (uint32_t)sizeof(T) / 4);
     static constexpr uint32_t RBUDGET = 2 * DATA > 255                ? 255
                                         : 2 * DATA < WG_RBUDGET_MIN ? WG_RBUDGET_MIN
