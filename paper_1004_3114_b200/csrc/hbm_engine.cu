@@ -446,182 +446,179 @@ __global__ void __launch_bounds__(kSumCta) k_sum_segs(KernelArgs a, uint32_t buf
 }
 
 constexpr uint32_t kWalkThreads = 256;
-constexpr uint32_t kBlockTerms = 32 * kSumChunk;
-constexpr uint32_t kMaxPre = 8;  // blocks whose terms the walk pre-stages
-#ifndef WG_WARP_WALK  // 1: warp 0 applies blocks / chunks 32 at a time
-#define WG_WARP_WALK 1
-#endif
+constexpr uint32_t kMaxPreBlk = 64;    // blocks whose chunk functions the walk pre-stages
+constexpr uint32_t kMaxPreChk = 128;   // chunks whose terms the walk pre-stages
 
+// The serial walk of the exact sum (one CTA).  Warp 0 applies the 32-chunk
+// block functions 32 at a time (warp_seg_walk); where a block cannot be
+// applied it walks the block's chunk functions, and where a chunk cannot be
+// applied lane 0 adds its 64 terms one by one.  Those places are predictable:
+// a block or chunk whose function is invalid (its guessed binade changes
+// inside it) — about one per power of two the sum crosses.  So before the
+// walk the whole CTA pre-stages, in one burst, the chunk functions of every
+// invalid block and the terms of every invalid chunk in them (64 terms each);
+// anything else that fails (a guess off by one binade) is fetched by warp 0
+// on demand: 32 chunk functions or 64 terms, one round trip.
 // mode 0: drift_check (compare, adopt or flag ECORRUPT); mode 1: set tracked.
 template <typename T>
 __global__ void __launch_bounds__(kWalkThreads) k_sum_walk(KernelArgs a, uint32_t buf,
                                                            uint64_t nvals, const SumSeg* segs,
                                                            const SumSeg* blocks, uint32_t nch,
-                                                           int mode, uint32_t maxpre) {
+                                                           int mode, uint32_t maxpb,
+                                                           uint32_t maxpc) {
     extern __shared__ __align__(16) unsigned char wsm[];
-    const uint32_t nblk = (nch + 31) / 32, nsup = (nblk + 31) / 32;
-    SumSeg* sblk = reinterpret_cast<SumSeg*>(wsm);         // [nblk]
-    SumSeg* ssup = sblk + nblk;                             // [nsup]
-    SumSeg* schk = ssup + nsup;                             // [32]
-    double* sterm = reinterpret_cast<double*>(schk + 32);   // [kBlockTerms]
-    double* spre = sterm + kBlockTerms;                     // [maxpre][kBlockTerms]
-    SumSeg* spchk = reinterpret_cast<SumSeg*>(spre + (size_t)maxpre * kBlockTerms);  // [maxpre][32]
-    __shared__ uint32_t s_fail;
-    __shared__ double s_q;
-    __shared__ uint32_t s_pre[kMaxPre], s_npre, s_wcnt[kWalkThreads / 32];
+    const uint32_t nblk = (nch + 31) / 32;
+    SumSeg* sblk = reinterpret_cast<SumSeg*>(wsm);                     // [nblk]
+    SumSeg* spchk = sblk + nblk;                                       // [maxpb][32]
+    SumSeg* schk = spchk + (size_t)maxpb * 32;                         // [32] on demand
+    double* spre = reinterpret_cast<double*>(schk + 32);               // [maxpc][kSumChunk]
+    double* sterm = spre + (size_t)maxpc * kSumChunk;                  // [kSumChunk] on demand
+    SumSeg* srun = reinterpret_cast<SumSeg*>(sterm + kSumChunk);       // [maxpb + 1]
+    __shared__ uint32_t s_pb[kMaxPreBlk], s_pc[kMaxPreChk], s_npb, s_npc;
+    __shared__ uint32_t s_wcnt[kWalkThreads / 32];
     if (a.meta->error) return;
     const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
+    const T* v = static_cast<const T*>(a.buf[buf]);
+    const HbmSplit sp = hbm_split(a.N);
     for (uint32_t b = t; b < nblk; b += kWalkThreads) sblk[b] = blocks[b];
-    if (t == 0) s_npre = 0;
+    if (t == 0) s_npb = s_npc = 0;
     __syncthreads();
-    // Pre-stage the terms of the first blocks whose function is invalid (a
-    // guessed binade changes inside them): the walk fails exactly there
-    // unless a guess was off, and one burst of loads replaces a latency-
-    // bound staging round per failure.  In block order (ballot compaction).
-    for (uint32_t base = 0; base < nblk && s_npre < maxpre; base += kWalkThreads) {
-        const uint32_t b = base + t;
-        const bool cand = b < nblk && !sblk[b].valid;
-        const uint32_t m = __ballot_sync(0xffffffffu, cand);
-        if (lane == 0) s_wcnt[warp] = __popc(m);
-        __syncthreads();
-        uint32_t off = s_npre;
-        for (uint32_t w = 0; w < warp; ++w) off += s_wcnt[w];
-        const uint32_t pos = off + __popc(m & ((1u << lane) - 1u));
-        if (cand && pos < maxpre) s_pre[pos] = b;
-        __syncthreads();
-        if (t == 0) {
-            uint32_t tot = s_npre;
-            for (uint32_t w = 0; w < kWalkThreads / 32; ++w) tot += s_wcnt[w];
-            s_npre = tot < maxpre ? tot : maxpre;
+    // ballot compaction of candidates in index order into list[<= cap]
+    auto compact = [&](uint32_t n, uint32_t cap, uint32_t* list, uint32_t& count, auto&& cand_of,
+                       auto&& id_of) {
+        for (uint32_t base = 0; base < n && count < cap; base += kWalkThreads) {
+            const uint32_t i = base + t;
+            const bool cand = i < n && cand_of(i);
+            const uint32_t m = __ballot_sync(0xffffffffu, cand);
+            if (lane == 0) s_wcnt[warp] = __popc(m);
+            __syncthreads();
+            uint32_t off = count;
+            for (uint32_t w = 0; w < warp; ++w) off += s_wcnt[w];
+            const uint32_t pos = off + __popc(m & ((1u << lane) - 1u));
+            if (cand && pos < cap) list[pos] = id_of(i);
+            __syncthreads();
+            if (t == 0) {
+                uint32_t tot = count;
+                for (uint32_t w = 0; w < kWalkThreads / 32; ++w) tot += s_wcnt[w];
+                count = tot < cap ? tot : cap;
+            }
+            __syncthreads();
         }
-        __syncthreads();
+    };
+    compact(nblk, maxpb, s_pb, s_npb, [&](uint32_t b) { return !sblk[b].valid; },
+            [](uint32_t b) { return b; });
+    const uint32_t npb = s_npb;
+    for (uint32_t i = t; i < npb * 32; i += kWalkThreads) {
+        const uint32_t c = s_pb[i / 32] * 32 + (i & 31u);
+        if (c < nch) {
+            spchk[i] = segs[c];
+        } else {
+            seg_init(spchk[i], 0);
+            spchk[i].valid = 0;
+        }
     }
-    const uint32_t npre = s_npre;
-    {
-        const T* vv = static_cast<const T*>(a.buf[buf]);
-        const HbmSplit sp0 = hbm_split(a.N);
-        for (uint32_t j0 = 0; j0 < npre; j0 += 2) {  // two blocks' terms in flight
-            constexpr uint32_t kPer = kBlockTerms / kWalkThreads;
-            double tv[2][kPer];
-#pragma unroll
-            for (uint32_t h = 0; h < 2; ++h) {
-                const uint64_t lo = (uint64_t)s_pre[j0 + h < npre ? j0 + h : j0] * kBlockTerms;
-#pragma unroll
-                for (uint32_t k = 0; k < kPer; ++k) {
-                    const uint64_t i = lo + t + (uint64_t)k * kWalkThreads;
-                    tv[h][k] = j0 + h < npre && i < nvals ? pool_term(vv, i, a.N, sp0) : 0.0;
-                }
+    __syncthreads();
+    compact(npb * 32, maxpc, s_pc, s_npc,
+            [&](uint32_t i) { return s_pb[i / 32] * 32 + (i & 31u) < nch && !spchk[i].valid; },
+            [&](uint32_t i) { return s_pb[i / 32] * 32 + (i & 31u); });
+    const uint32_t npc = s_npc;
+    for (uint32_t i = t; i < npc * kSumChunk; i += kWalkThreads) {
+        const uint64_t term = (uint64_t)s_pc[i / kSumChunk] * kSumChunk + i % kSumChunk;
+        spre[i] = term < nvals ? pool_term(v, term, a.N, sp) : 0.0;
+    }
+    // Runs of blocks between consecutive pre-staged (invalid) blocks, each
+    // composed into one function in parallel (a warp per run, 32 blocks per
+    // step by a shuffle scan), so the serial walk applies a whole run at once.
+    for (uint32_t r = warp; r <= npb; r += kWalkThreads / 32) {
+        const uint32_t lo = r == 0 ? 0u : s_pb[r - 1] + 1, hi = r < npb ? s_pb[r] : nblk;
+        SumSeg acc;
+        seg_init(acc, lo < hi ? sblk[lo].e : 0);
+        for (uint32_t base = lo; base < hi; base += 32) {
+            SumSeg g;
+            if (base + lane < hi) {
+                g = sblk[base + lane];
+            } else {
+                seg_init(g, acc.e);  // identity in the run's binade
             }
 #pragma unroll
-            for (uint32_t h = 0; h < 2; ++h)
-                if (j0 + h < npre)
-#pragma unroll
-                    for (uint32_t k = 0; k < kPer; ++k)
-                        spre[(size_t)(j0 + h) * kBlockTerms + t + k * kWalkThreads] = tv[h][k];
+            for (uint32_t o = 1; o < 32; o <<= 1) {
+                const SumSeg y = seg_shfl_up(g, o);
+                if (lane >= o) g = seg_compose(y, g);
+            }
+            SumSeg tot;
+            tot.s[0] = __shfl_sync(0xffffffffu, g.s[0], 31);
+            tot.s[1] = __shfl_sync(0xffffffffu, g.s[1], 31);
+            tot.par[0] = __shfl_sync(0xffffffffu, g.par[0], 31);
+            tot.par[1] = __shfl_sync(0xffffffffu, g.par[1], 31);
+            tot.valid = __shfl_sync(0xffffffffu, g.valid, 31);
+            tot.e = __shfl_sync(0xffffffffu, g.e, 31);
+            acc = seg_compose(acc, tot);
         }
-        for (uint32_t i = t; i < npre * 32; i += kWalkThreads) {
-            const uint32_t c = s_pre[i / 32] * 32 + (i & 31u);
-            if (c < nch) spchk[i] = segs[c];
+        if (lane == 0) {
+            seg_finalize(acc);
+            srun[r] = acc;
         }
-    }
-    __syncthreads();
-    for (uint32_t u = t; u < (WG_WARP_WALK ? 0u : nsup); u += kWalkThreads) {  // super-blocks
-        SumSeg g = sblk[u * 32];
-        const uint32_t end = u * 32 + 32 < nblk ? u * 32 + 32 : nblk;
-        for (uint32_t b = u * 32 + 1; b < end; ++b) g = seg_compose(g, sblk[b]);
-        if (u * 32 + 32 > nblk) g.valid = 0;
-        seg_finalize(g);
-        ssup[u] = g;
     }
     __syncthreads();
     for (uint32_t b = t; b < nblk; b += kWalkThreads) seg_finalize(sblk[b]);
-    const T* v = static_cast<const T*>(a.buf[buf]);
-    const HbmSplit sp = hbm_split(a.N);
-    if (t == 0) s_q = 0.0;
     __syncthreads();
-    uint32_t b0 = 0;  // next block to apply
-    while (true) {
-        if (WG_WARP_WALK) {
-            // warp 0: blocks 32 at a time (prefix compositions tried at once)
-            if (warp == 0) {
-                double q = s_q;
-                const uint32_t cnt = warp_seg_walk(q, nblk - b0, [&](uint32_t k) {
-                    return seg_unfinalize(sblk[b0 + k]);
-                });
-                if (t == 0) {
-                    s_q = q;
-                    s_fail = b0 + cnt;
-                }
-            }
-        } else if (t == 0) {
-            double q = s_q;
-            uint32_t b = b0;
-            while (b < nblk) {
-                if ((b & 31) == 0 && seg_apply(q, ssup[b >> 5])) {
-                    b += 32;
-                    continue;
-                }
-                if (!seg_apply(q, sblk[b])) break;
-                ++b;
-            }
-            s_q = q;
-            s_fail = b;
+    if (warp != 0) return;
+    // ---- warp 0: the serial walk --------------------------------------
+    // index of `id` in list[0, n), or n (lanes search 32 entries at a time)
+    auto find = [&](const uint32_t* list, uint32_t n, uint32_t id) -> uint32_t {
+        for (uint32_t base = 0; base < n; base += 32) {
+            const uint32_t m =
+                __ballot_sync(0xffffffffu, base + lane < n && list[base + lane] == id);
+            if (m) return base + (uint32_t)__ffs(m) - 1u;
         }
-        __syncthreads();
-        const uint32_t fb = s_fail;
-        if (fb >= nblk) break;
-        // the failing block's chunk functions and terms: pre-staged, or
-        // staged now
-        const uint32_t c0 = fb * 32, cend = c0 + 32 < nch ? c0 + 32 : nch;
-        const uint64_t lo = (uint64_t)c0 * kSumChunk, hi = umin64(lo + kBlockTerms, nvals);
-        uint32_t jp = npre;
-        for (uint32_t j = 0; j < npre; ++j)
-            if (s_pre[j] == fb) jp = j;
-        const SumSeg* ck = schk;
-        const double* tm = sterm;
-        if (jp < npre) {
-            ck = spchk + (size_t)jp * 32;
-            tm = spre + (size_t)jp * kBlockTerms;
-        } else {
-            if (t < cend - c0) schk[t] = segs[c0 + t];
-            for (uint64_t i = lo + t; i < hi; i += kWalkThreads)
-                sterm[i - lo] = pool_term(v, i, a.N, sp);
-            __syncthreads();
+        return n;
+    };
+    double q = 0.0;
+    // blocks [b, hi) one at a time where a run function does not apply
+    auto walk_blocks = [&](uint32_t b, uint32_t hi) {
+      while (b < hi) {
+        b += warp_seg_walk(q, hi - b, [&](uint32_t k) { return seg_unfinalize(sblk[b + k]); });
+        if (b >= hi) break;
+        // block b cannot be applied: its chunk functions
+        const uint32_t c0 = b * 32, cend = c0 + 32 < nch ? c0 + 32 : nch;
+        const uint32_t jb = find(s_pb, npb, b);
+        const SumSeg* ck = spchk + (size_t)jb * 32;
+        if (jb >= npb) {
+            if (c0 + lane < cend) schk[lane] = segs[c0 + lane];
+            __syncwarp();
+            ck = schk;
         }
-        if (WG_WARP_WALK) {
-            if (warp == 0) {  // chunks 32 at a time; a failing chunk's terms on lane 0
-                double q = s_q;
-                uint32_t c = c0;
-                while (c < cend) {
-                    const uint32_t cs = c;
-                    c += warp_seg_walk(q, cend - cs, [&](uint32_t k) {
-                        return seg_unfinalize(ck[cs - c0 + k]);
-                    });
-                    if (c >= cend) break;
-                    if (lane == 0) {
-                        const uint64_t l2 = (uint64_t)c * kSumChunk,
-                                       h2 = umin64(l2 + kSumChunk, nvals);
-                        for (uint64_t i = l2; i < h2; ++i) q = q + tm[i - lo];
-                    }
-                    q = __shfl_sync(0xffffffffu, q, 0);
-                    ++c;
-                }
-                if (t == 0) s_q = q;
+        uint32_t c = c0;
+        while (c < cend) {
+            const uint32_t cs = c;
+            c += warp_seg_walk(q, cend - cs, [&](uint32_t k) { return seg_unfinalize(ck[cs - c0 + k]); });
+            if (c >= cend) break;
+            // chunk c cannot be applied: its terms, one by one
+            const uint64_t l2 = (uint64_t)c * kSumChunk, h2 = umin64(l2 + kSumChunk, nvals);
+            const uint32_t jc = find(s_pc, npc, c);
+            const double* tm = spre + (size_t)jc * kSumChunk;
+            if (jc >= npc) {
+#pragma unroll
+                for (uint32_t h = 0; h < kSumChunk; h += 32)
+                    if (l2 + h + lane < h2) sterm[h + lane] = pool_term(v, l2 + h + lane, a.N, sp);
+                __syncwarp();
+                tm = sterm;
             }
-        } else if (t == 0) {
-            double q = s_q;
-            for (uint32_t c = c0; c < cend; ++c) {
-                if (seg_apply(q, ck[c - c0])) continue;
-                const uint64_t l2 = (uint64_t)c * kSumChunk, h2 = umin64(l2 + kSumChunk, nvals);
-                for (uint64_t i = l2; i < h2; ++i) q = q + tm[i - lo];
-            }
-            s_q = q;
+            if (lane == 0)
+                for (uint64_t i = l2; i < h2; ++i) q = q + tm[i - l2];
+            q = __shfl_sync(0xffffffffu, q, 0);
+            __syncwarp();  // sterm / schk reused
+            ++c;
         }
-        b0 = fb + 1;
-        __syncthreads();
+        ++b;
+      }
+    };
+    for (uint32_t r = 0; r <= npb; ++r) {
+        const uint32_t lo = r == 0 ? 0u : s_pb[r - 1] + 1, hi = r < npb ? s_pb[r] : nblk;
+        if (hi > lo && !seg_apply(q, srun[r])) walk_blocks(lo, hi);
+        if (r < npb) walk_blocks(hi, hi + 1);  // the invalid block itself
     }
-    if (t != 0) return;
-    const double q = s_q;
+    if (lane != 0) return;
     if (mode == 1) {
         a.meta->tracked[buf] = q;
         return;
@@ -682,15 +679,19 @@ static cudaError_t exact_sum(uint32_t dtype, const KernelArgs& a, uint32_t buf, 
     SumSeg* segs = reinterpret_cast<SumSeg*>(
         (reinterpret_cast<uintptr_t>(cta_sum + ncta) + 63) & ~uintptr_t(63));
     SumSeg* blocks = segs + nch;
-    const uint32_t nblk = (nch + 31) / 32, nsup = (nblk + 31) / 32;
-    const size_t wbase = (nblk + nsup + 32) * sizeof(SumSeg) + kBlockTerms * sizeof(double);
-    // pre-staged blocks: as many (<= kMaxPre) as fit next to the rest
-    const size_t pre_each = kBlockTerms * sizeof(double) + 32 * sizeof(SumSeg);
+    const uint32_t nblk = (nch + 31) / 32;
+    const size_t wbase = (nblk + 32) * sizeof(SumSeg) + kSumChunk * sizeof(double);
+    // pre-staged block functions (32 chunks each) and chunk terms, two
+    // chunks per block, as many as fit next to the block functions
     const size_t kWalkSmemMax = 200 * 1024;
-    const uint32_t maxpre = wbase + pre_each > kWalkSmemMax
-                                ? 0u
-                                : (uint32_t)std::min<size_t>(kMaxPre, (kWalkSmemMax - wbase) / pre_each);
-    const size_t wsm = wbase + maxpre * pre_each;
+    const size_t pre_pair = 33 * sizeof(SumSeg) + 2 * kSumChunk * sizeof(double);
+    const uint32_t maxpb =
+        wbase + pre_pair > kWalkSmemMax
+            ? 0u
+            : (uint32_t)std::min<size_t>(kMaxPreBlk, (kWalkSmemMax - wbase) / pre_pair);
+    const uint32_t maxpc = std::min<uint32_t>(kMaxPreChk, 2 * maxpb);
+    const size_t wsm = wbase + (size_t)maxpb * 32 * sizeof(SumSeg) +
+                       (size_t)maxpc * kSumChunk * sizeof(double) + (maxpb + 1) * sizeof(SumSeg);
     cudaFuncSetAttribute(k_sum_walk<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)wsm);
     cudaFuncSetAttribute(k_sum_walk<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -700,13 +701,13 @@ static cudaError_t exact_sum(uint32_t dtype, const KernelArgs& a, uint32_t buf, 
         k_sum_segs<double><<<ncta, kSumCta, 0, st>>>(a, buf, nvals, pre_local, cta_sum, segs,
                                                      blocks, nch);
         k_sum_walk<double><<<1, kWalkThreads, wsm, st>>>(a, buf, nvals, segs, blocks, nch, mode,
-                                                         maxpre);
+                                                         maxpb, maxpc);
     } else {
         k_sum_chunks<float><<<ncta, kSumCta, 0, st>>>(a, buf, nvals, pre_local, cta_sum, nch);
         k_sum_segs<float><<<ncta, kSumCta, 0, st>>>(a, buf, nvals, pre_local, cta_sum, segs,
                                                     blocks, nch);
         k_sum_walk<float><<<1, kWalkThreads, wsm, st>>>(a, buf, nvals, segs, blocks, nch, mode,
-                                                        maxpre);
+                                                        maxpb, maxpc);
     }
     return cudaGetLastError();
 }
