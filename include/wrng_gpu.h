@@ -163,6 +163,12 @@ wrng_gpu_status wrng_gpu_read_uniform(wrng_gpu_t* g, uint32_t pool, uint64_t* ta
                                       uint32_t* cursor_r, uint32_t* cursor_s,
                                       uint64_t* draws);
 
+/* Overwrites pool `pool`'s uniform generator (the mutable uniform_state(),
+ * wallace.hpp:158).  EINVAL unless cursor_r < 607 and
+ * cursor_s = (cursor_r + 334) mod 607 (serialize.cpp:145-148). */
+wrng_gpu_status wrng_gpu_write_uniform(wrng_gpu_t* g, uint32_t pool, const uint64_t* table607,
+                                       uint32_t cursor_r, uint32_t cursor_s, uint64_t draws);
+
 /* save_state / load_state (serialize.cpp:82-169).  A handle with n = 2,
  * f64, 1 pool exports the reference's "WRNG" v1 bytes exactly; anything else
  * exports v2 (docs/n4_spec.md §6).  export: *size receives the byte count;

@@ -26,7 +26,8 @@
 //     test_wallace_state.cpp:128-150) are written back to the device before
 //     the next operation.  A reference held across a later operation keeps
 //     the older contents (the reference's would alias the other buffer).
-//   * uniform_state() returns a snapshot of the device generator's state.
+//   * uniform_state() is likewise a host view of the device generator;
+//     draws made through it are written back before the next operation.
 //   * WallaceState is copyable (a deep copy through save_state/load_state).
 // Free functions on value-type pools run regenerate on the GPU
 // (wrng_gpu_regenerate) and the scalar parts in libwrng_gpu.so, built with
@@ -281,9 +282,10 @@ public:
     }
     WallaceState(WallaceState&& o) noexcept
         : g_(o.g_), cfg_(o.cfg_), view_(std::move(o.view_)), shadow_(std::move(o.shadow_)),
-          view_valid_(o.view_valid_), lent_(o.lent_) {
+          view_valid_(o.view_valid_), lent_(o.lent_), uview_(o.uview_), ushadow_(o.ushadow_),
+          uview_valid_(o.uview_valid_), ulent_(o.ulent_) {
         o.g_ = nullptr;
-        o.view_valid_ = o.lent_ = false;
+        o.view_valid_ = o.lent_ = o.uview_valid_ = o.ulent_ = false;
     }
     WallaceState& operator=(WallaceState&& o) noexcept {
         if (this != &o) {
@@ -294,8 +296,12 @@ public:
             shadow_ = std::move(o.shadow_);
             view_valid_ = o.view_valid_;
             lent_ = o.lent_;
+            uview_ = o.uview_;
+            ushadow_ = o.ushadow_;
+            uview_valid_ = o.uview_valid_;
+            ulent_ = o.ulent_;
             o.g_ = nullptr;
-            o.view_valid_ = o.lent_ = false;
+            o.view_valid_ = o.lent_ = o.uview_valid_ = o.ulent_ = false;
         }
         return *this;
     }
@@ -433,17 +439,26 @@ public:
         detail::check(wrng_gpu_write_pool(g_, pool, v.data(), p.tracked_sumsq, p.withheld), g_,
                       "set_active_pool");
     }
-    /// Snapshot of the device uniform generator of `pool` (the reference
-    /// returns a reference into the state; advancing this copy does not
-    /// advance the generator).
-    UniformState uniform_state(std::uint32_t pool = 0) const {
+    /// The live uniform generator (of pool 0) as a host view, like
+    /// active_pool(): draws made through it are written back to the device
+    /// before the next operation (wallace.hpp:158).
+    UniformState& uniform_state() {
+        refresh_uview();
+        if (!ulent_) {
+            ushadow_ = uview_;
+            ulent_ = true;
+        }
+        return uview_;
+    }
+    const UniformState& uniform_state() const {
+        refresh_uview();
+        return uview_;
+    }
+    /// Snapshot of pool `pool`'s uniform generator (banks).
+    UniformState uniform_state(std::uint32_t pool) const {
         flush();
         UniformState u;
-        detail::check(wrng_gpu_read_uniform(g_, pool, u.lag_table.data(), &u.cursor_r,
-                                            &u.cursor_s, &u.draws),
-                      g_, "uniform_state");
-        u.seed = cfg_.seed;
-        u.stream_id = cfg_.stream_id + pool;
+        read_uniform(pool, u);
         return u;
     }
     wrng_gpu_t* handle() const { return g_; }
@@ -486,14 +501,36 @@ private:
         for (std::uint32_t m = 0; m < na; ++m)
             p.array(m).assign(v.begin() + std::size_t(m) * n, v.begin() + std::size_t(m + 1) * n);
     }
+    void read_uniform(std::uint32_t pool, UniformState& u) const {
+        detail::check(wrng_gpu_read_uniform(g_, pool, u.lag_table.data(), &u.cursor_r,
+                                            &u.cursor_s, &u.draws),
+                      g_, "uniform_state");
+        u.seed = cfg_.seed;
+        u.stream_id = cfg_.stream_id + pool;
+    }
+    void refresh_uview() const {
+        if (uview_valid_) return;
+        read_uniform(0, uview_);
+        uview_valid_ = true;
+        ulent_ = false;
+    }
     void refresh_view() const {
         if (view_valid_) return;
         read_pool(0, view_);
         view_valid_ = true;
         lent_ = false;
     }
-    /// Writes back edits made through active_pool() since it was read.
+    /// Writes back edits made through active_pool() / uniform_state()
+    /// since they were read.
     void flush() const {
+        if (ulent_) {
+            ulent_ = false;
+            if (std::memcmp(&uview_, &ushadow_, sizeof(UniformState)) != 0)
+                detail::check(wrng_gpu_write_uniform(g_, 0, uview_.lag_table.data(),
+                                                     uview_.cursor_r, uview_.cursor_s,
+                                                     uview_.draws),
+                              g_, "uniform_state (write back)");
+        }
         if (!lent_) return;
         lent_ = false;
         bool same = view_.n_arrays() == shadow_.n_arrays() &&
@@ -519,6 +556,7 @@ private:
     void begin_op() {
         flush();
         view_valid_ = false;
+        uview_valid_ = false;
     }
 
     wrng_gpu_t* g_ = nullptr;
@@ -527,6 +565,10 @@ private:
     mutable Pool shadow_;
     mutable bool view_valid_ = false;
     mutable bool lent_ = false;
+    mutable UniformState uview_{};
+    mutable UniformState ushadow_{};
+    mutable bool uview_valid_ = false;
+    mutable bool ulent_ = false;
 };
 
 // ---- diagnostic pool streams (wallace.hpp:176-191; wallace.cpp:238-291) ----

@@ -108,6 +108,7 @@ EXPORTS = (
     "wrng_gpu_normal_fill", "wrng_gpu_to_uv", "wrng_gpu_chi2_bins", "wrng_gpu_moments_host",
     "wrng_gpu_autocorr_host", "wrng_gpu_target_stats",
     "wrng_gpu_validate_ex", "wrng_gpu_anderson_darling", "wrng_gpu_resident_pools",
+    "wrng_gpu_write_uniform",
 )
 
 
@@ -186,6 +187,7 @@ def _load():
         "wrng_gpu_validate_ex": (C.c_int, [vp, u64, u32, u64, u32, vp, vp, P(Validation)]),
         "wrng_gpu_anderson_darling": (C.c_int, [vp, i32, u64, P(dbl), i32, vp]),
         "wrng_gpu_resident_pools": (C.c_int64, [P(Config)]),
+        "wrng_gpu_write_uniform": (C.c_int, [vp, u32, vp, u32, u32, u64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

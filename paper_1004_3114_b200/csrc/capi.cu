@@ -1320,6 +1320,32 @@ static wrng_gpu_status read_uniform_impl(wrng_gpu_t* g, uint32_t pool, uint64_t*
     return WRNG_GPU_OK;
 }
 
+static wrng_gpu_status write_uniform_impl(wrng_gpu_t* g, uint32_t pool, const uint64_t* table607,
+                                          uint32_t cursor_r, uint32_t cursor_s, uint64_t draws) {
+    if (!g || !table607 || pool >= g->cfg.pools) return WRNG_GPU_EINVAL;
+    if (cursor_r >= kTable || (cursor_r + kGap) % kTable != cursor_s)
+        return fail(g, WRNG_GPU_EINVAL, "write_uniform: cursors out of range");
+    DeviceGuard dg(g->cfg.device);
+    wrng_gpu_status st = collect(g);
+    if (st) return st;
+    ++g->gen;
+    LfgState l;
+    std::memcpy(l.table, table607, sizeof(l.table));
+    l.r = cursor_r;
+    l.pad_ = 0;
+    l.draws = draws;
+    CK(cudaMemcpyAsync(g->lfg + pool, &l, sizeof(l), cudaMemcpyHostToDevice, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    return WRNG_GPU_OK;
+}
+
+wrng_gpu_status wrng_gpu_write_uniform(wrng_gpu_t* g, uint32_t pool, const uint64_t* table607,
+                                       uint32_t cursor_r, uint32_t cursor_s, uint64_t draws) {
+    return guarded(g, [&] {
+        return write_uniform_impl(g, pool, table607, cursor_r, cursor_s, draws);
+    });
+}
+
 wrng_gpu_status wrng_gpu_read_uniform(wrng_gpu_t* g, uint32_t pool, uint64_t* table607,
                                       uint32_t* cursor_r, uint32_t* cursor_s,
                                       uint64_t* draws) {

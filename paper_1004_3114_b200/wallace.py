@@ -439,6 +439,13 @@ class WallaceState:
                                          C.byref(d)), "uniform_state", self._h)
         return UniformStateView(t, r.value, s.value, d.value)
 
+    def set_uniform_state(self, u: UniformStateView, pool: int = 0):
+        """Overwrites the device uniform generator (the reference's mutable
+        uniform_state(), wallace.hpp:158)."""
+        t = np.ascontiguousarray(u.lag_table, dtype=np.uint64)
+        _raise(lib.wrng_gpu_write_uniform(self._h, pool, t.ctypes.data, u.cursor_r, u.cursor_s,
+                                          u.draws), "set_uniform_state", self._h)
+
     def kernel_launches(self) -> int:
         return int(lib.wrng_gpu_kernel_launches(self._h))
 

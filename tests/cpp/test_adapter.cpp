@@ -230,6 +230,27 @@ int main() {
         CHECK(p.strides[2] == 13 || p.strides[2] == 17);
         CHECK(p.variant <= 1);
     }
+    // the mutable uniform_state() (wallace.hpp:158): draws made through it
+    // advance the generator, as in the reference; copies are deep
+    {
+        WallaceState a(config_with(1, ScaleMode::chisq, 3)), b(config_with(1, ScaleMode::chisq, 3)),
+            c(config_with(1, ScaleMode::chisq, 3));
+        a.fill(5000);
+        b.fill(5000);
+        c.fill(5000);
+        for (int i = 0; i < 3; ++i) {
+            a.uniform_state().next_word();
+            b.uniform_state().next_word();
+        }
+        CHECK(a.uniform_state().draws == c.uniform_state().draws);  // next_word is not a draw
+        PassParams pa = a.advance_pass(), pb = b.advance_pass(), pc = c.advance_pass();
+        CHECK(pa.gamma == pb.gamma && pa.delta == pb.delta && pa.rot.c == pb.rot.c);
+        CHECK(pa.gamma != pc.gamma || pa.delta != pc.delta || pa.rot.c != pc.rot.c);
+        WallaceState d = a;  // copy
+        auto va = a.fill(3000);
+        auto vd = d.fill(3000);
+        CHECK(va == vd);
+    }
     std::printf("adapter checks: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;
 }

@@ -744,6 +744,28 @@ def test_state_after_mid_fill_audit_failure_matches_oracle(W, force_hbm, n, f):
     assert (gp.tracked_sumsq, gp.withheld) == (pt, pw)
 
 
+@pytest.mark.parametrize("force_hbm", [False, True])
+def test_uniform_state_write_back(W, force_hbm):
+    """The mutable uniform_state() (wallace.hpp:158): a generator whose
+    uniform state is overwritten with another stream's draws that stream's
+    pass parameters next; malformed cursors are rejected."""
+    a = gpu_state(W, pool_exponent=10, seed=5, force_hbm=force_hbm)
+    b = gpu_state(W, pool_exponent=10, seed=9, force_hbm=force_hbm)
+    a.fill(3000)
+    b.fill(5000)
+    a.set_uniform_state(b.uniform_state())
+    ua, ub = a.uniform_state(), b.uniform_state()
+    assert_bits(ua.lag_table, ub.lag_table)
+    assert (ua.cursor_r, ua.cursor_s, ua.draws) == (ub.cursor_r, ub.cursor_s, ub.draws)
+    pa, pb = a.advance_pass(), b.advance_pass()
+    assert (pa.alpha, pa.beta, pa.gamma, pa.delta, pa.rot.c, pa.rot.s) == (
+        pb.alpha, pb.beta, pb.gamma, pb.delta, pb.rot.c, pb.rot.s)
+    bad = b.uniform_state()
+    bad.cursor_s = (bad.cursor_r + 1) % 607
+    with pytest.raises(ValueError):
+        a.set_uniform_state(bad)
+
+
 def test_zero_tracked_sum_raises(W):
     g = gpu_state(W, pool_exponent=10, seed=3)
     p = g.active_pool()
