@@ -641,7 +641,7 @@ wrng_gpu_status run_hbm(wrng_gpu* g, uint32_t p, Ctr c, const std::vector<Ev>& e
 
 // One device-output bank fill (no staging): `lay` places each pool's values.
 wrng_gpu_status fill_device(wrng_gpu* g, void* out, int out_f32, const OutLayout& lay,
-                            double mu, double sigma, cudaStream_t s) {
+                            double mu, double sigma, cudaStream_t s, double* stats = nullptr) {
     const uint32_t P = g->cfg.pools;
     const bool unit = mu == 0.0 && sigma == 1.0;
     wrng_gpu_status st = order_on(g, s);
@@ -659,7 +659,8 @@ wrng_gpu_status fill_device(wrng_gpu* g, void* out, int out_f32, const OutLayout
                           ? g_bulk_align
                           : 0u;
         a.host_restart = host_bm(g) && g->cfg.restart_interval_passes > 0;
-        if (g_cluster && g->cfg.restart_interval_passes == 0 &&
+        a.stats = stats;
+        if (g_cluster && !stats && g->cfg.restart_interval_passes == 0 &&
             cluster_engine_fits(g->cfg.n_arrays, g->cfg.dtype, g->N, P))
             LAUNCH(launch_cluster(g->cfg.n_arrays, g->cfg.dtype, a, s));
         else
@@ -1683,9 +1684,11 @@ struct StatBufs {
     unsigned long long* cnt = nullptr;  // [k] u, [k] v, [1] skipped
     void* tail[2] = {nullptr, nullptr};
     void* ad = nullptr;  // A^2 keys + sort scratch
+    double* pst = nullptr;  // [pools][4] moment sums of the fused path
     static constexpr uint32_t kBlocks = 148 * 4;
     ~StatBufs() {
         cudaFree(ad);
+        cudaFree(pst);
         cudaFree(part);
         cudaFree(acc);
         cudaFree(cnt);
@@ -1793,6 +1796,13 @@ static wrng_gpu_status validate_impl(wrng_gpu_t* g, uint64_t count, uint32_t k, 
         }
     }
     uint64_t ad_at = 0;
+    // smem engine: the moment sums are accumulated by the emitting passes
+    // themselves (per pool, fixed order); the HBM engine reduces the slab
+    const bool fused = !g->hbm;
+    if (fused) {
+        CK(cudaMalloc(&b.pst, sizeof(double) * 4 * P));
+        CK(cudaMemsetAsync(b.pst, 0, sizeof(double) * 4 * P, s));
+    }
     // windows of L values per pool (even: pairs never straddle windows), the
     // slab kept <= 64 MiB so the reductions re-read it from L2
     const uint64_t slab = std::min<uint64_t>(g->stage_bytes, (uint64_t)64 << 20) / esz;
@@ -1806,7 +1816,7 @@ static wrng_gpu_status validate_impl(wrng_gpu_t* g, uint64_t count, uint32_t k, 
         lay.len_base = tail ? base - t : L;
         lay.len_extra = tail ? extra : 0;
         if (lay.len_base == 0 && lay.len_extra == 0) break;
-        st = fill_device(g, g->stage[0], f32, lay, 0.0, 1.0, s);
+        st = fill_device(g, g->stage[0], f32, lay, 0.0, 1.0, s, fused ? b.pst : nullptr);
         if (st) return st;
         // groups of equal window length: [0, len_extra) one longer
         struct Grp {
@@ -1817,7 +1827,9 @@ static wrng_gpu_status validate_impl(wrng_gpu_t* g, uint64_t count, uint32_t k, 
         for (const Grp& gr : grp) {
             if (gr.np == 0 || gr.len == 0) continue;
             const char* w = static_cast<const char*>(g->stage[0]) + (size_t)gr.p0 * L * esz;
-            CK(launch_moment_sums(w, f32, gr.np, L, gr.len, b.part, StatBufs::kBlocks, b.acc, s));
+            if (!fused)
+                CK(launch_moment_sums(w, f32, gr.np, L, gr.len, b.part, StatBufs::kBlocks, b.acc,
+                                      s));
             if (want_ad) {
                 CK(ad_add_values(w, f32, gr.np, L, gr.len, b.ad, ad_at, s));
                 ad_at += (uint64_t)gr.np * gr.len;
@@ -1846,6 +1858,14 @@ static wrng_gpu_status validate_impl(wrng_gpu_t* g, uint64_t count, uint32_t k, 
     std::vector<unsigned long long> h(2 * k + 1);
     CK(cudaStreamSynchronize(s));
     if (want_ad) CK(cudaMemcpy(&a2, b.acc + 8, sizeof(double), cudaMemcpyDeviceToHost));
+    if (fused) {  // pools in order
+        std::vector<double> ps(4 * (size_t)P);
+        CK(cudaMemcpy(ps.data(), b.pst, sizeof(double) * ps.size(), cudaMemcpyDeviceToHost));
+        double sum[4] = {0.0, 0.0, 0.0, 0.0};
+        for (uint32_t p = 0; p < P; ++p)
+            for (int k = 0; k < 4; ++k) sum[k] += ps[4 * (size_t)p + k];
+        CK(cudaMemcpy(b.acc, sum, sizeof(sum), cudaMemcpyHostToDevice));
+    }
     CK(cudaMemcpy(acc, b.acc, sizeof(acc), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(h.data(), b.cnt, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
     st = collect(g);

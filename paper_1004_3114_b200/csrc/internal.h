@@ -94,6 +94,9 @@ struct KernelArgs {
     // continue the pools the host restarted
     uint32_t host_restart;
     uint32_t resume;
+    // smem fills: non-null -> the emitting passes also add each pool's sums
+    // of v, v^2, v^3, v^4 over its emitted values to stats[pool * 4 + k]
+    double* stats;
 };
 
 struct EngineShape {

@@ -61,7 +61,9 @@ static constexpr uint32_t kSmemPoolMax = 128 * 1024;  // largest pool kept on ch
 
 extern __shared__ __align__(16) unsigned char g_sm[];
 
-enum EmitMode : int { EM_UNIT = 0, EM_GENERIC = 1 };
+// EM_STATS: generic emission that also accumulates the moment sums of every
+// emitted value (wrng_gpu_validate: s1..s4 fused into the emitting pass)
+enum EmitMode : int { EM_UNIT = 0, EM_GENERIC = 1, EM_STATS = 2 };
 
 #ifndef WG_RBUDGET_MIN  // smallest per-thread register budget of a shape (128 measured slower:
                         // 4x256 pools 32 % vs 37.5 % fp32, 66 % vs 81 % fp64)
@@ -165,6 +167,15 @@ __device__ __forceinline__ void emit_one(void* out, uint64_t i, T v, uint32_t ou
 struct EmitCfg {  // per-launch constants of the output stream
     double mu, sigma;
     uint32_t out_f32, unit;
+    // EM_STATS: this thread's sums of v, v^2, v^3, v^4 over its emitted values
+    mutable double st[4] = {0.0, 0.0, 0.0, 0.0};
+    __device__ __forceinline__ void add(double v) const {
+        const double v2 = v * v;
+        st[0] += v;
+        st[1] += v2;
+        st[2] += v2 * v;
+        st[3] += v2 * v2;
+    }
 };
 
 // ---- bulk-copy emission of full refills (unit output) ---------------------
@@ -540,9 +551,11 @@ __device__ __forceinline__ void phase_c2(const f2_t (&u)[4][SmemShape<float, 4, 
 #endif
                 } else if constexpr (MD == 2) {
                     const uint32_t flat = col + tid;
-                    if (flat < en)
+                    if (flat < en) {
                         emit_one<float, EM>(out_p, flat, y[h], ec.out_f32, ec.unit, ec.mu,
                                             ec.sigma);
+                        if constexpr (EM == EM_STATS) ec.add((double)y[h]);
+                    }
                 }
                 if (m == 3 && k == (int)S::J - 1 && tid == S::NTH - 1)
                     withheld_out = (double)y[h];
@@ -589,8 +602,10 @@ __device__ __forceinline__ void phase_c(const T (&u)[NA][SmemShape<T, NA, LOGN>:
                     ob[col] = y[m] + (T)0;  // 0 + 1 * v
             } else if constexpr (MD == 2) {
                 const uint32_t flat = col + tid;
-                if (flat < en)
+                if (flat < en) {
                     emit_one<T, EM>(out_p, flat, y[m], ec.out_f32, ec.unit, ec.mu, ec.sigma);
+                    if constexpr (EM == EM_STATS) ec.add((double)y[m]);
+                }
             }
         });
         if (k == (int)S::J - 1 && tid == S::NTH - 1) withheld_out = (double)y[NA - 1];
@@ -947,8 +962,10 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
         const uint64_t pos = CAP - avail;
         char* o = outc + out_base * esz;
         const T* pl = &sm_at<T>(S::POOL_OFF);
-        for (uint64_t i = tid; i < take; i += NTH)
+        for (uint64_t i = tid; i < take; i += NTH) {
             emit_one<T, EM>(o, i, pl[pos + i], ec.out_f32, ec.unit, ec.mu, ec.sigma);
+            if constexpr (EM == EM_STATS) ec.add((double)pl[pos + i]);
+        }
         done = take;
         avail -= take;
     }
@@ -1044,6 +1061,24 @@ __global__ void __launch_bounds__(SmemShape<T, NA, LOGN>::NTH, SmemShape<T, NA, 
     // ---- write back -------------------------------------------------------
     if (bulk_on && tid == 0) bulk_wait_all();  // bulk copies complete before exit
     __syncthreads();
+    if constexpr (EM == EM_STATS) {
+        // this pool's moment sums: lanes, then warps, in a fixed order
+        double* red = &sm_at<double>(S::WBUF_OFF);  // [warps][4]
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            double x = ec.st[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+            if ((tid & 31u) == 0) red[(tid >> 5) * 4 + k] = x;
+        }
+        __syncthreads();
+        if (tid < 4 && a.stats) {
+            double x = 0.0;
+            for (uint32_t w = 0; w < NTH / 32; ++w) x += red[w * 4 + tid];
+            a.stats[(uint64_t)p * 4 + tid] += x;
+        }
+        __syncthreads();
+    }
     const uint32_t act = ctl->active;
     if (ctl->rot == 0) {
         uint4* dst =
@@ -1098,11 +1133,13 @@ static cudaError_t go_em(const KernelArgs& a, cudaStream_t st, bool unit_same, b
     using S = SmemShape<T, NA, LOGN>;
     if constexpr (S::CAN_ALIGN) {
         if (al)
-            return unit_same ? go<T, NA, LOGN, EM_UNIT, true>(a, st)
-                             : go<T, NA, LOGN, EM_GENERIC, true>(a, st);
+            return a.stats      ? go<T, NA, LOGN, EM_STATS, true>(a, st)
+                   : unit_same ? go<T, NA, LOGN, EM_UNIT, true>(a, st)
+                               : go<T, NA, LOGN, EM_GENERIC, true>(a, st);
     }
-    return unit_same ? go<T, NA, LOGN, EM_UNIT, false>(a, st)
-                     : go<T, NA, LOGN, EM_GENERIC, false>(a, st);
+    return a.stats      ? go<T, NA, LOGN, EM_STATS, false>(a, st)
+           : unit_same ? go<T, NA, LOGN, EM_UNIT, false>(a, st)
+                       : go<T, NA, LOGN, EM_GENERIC, false>(a, st);
 }
 
 template <typename T, int NA>
