@@ -1021,7 +1021,7 @@ wrng_gpu_status alloc_handle(const wrng_gpu_config* cfg, wrng_gpu** out) {
     CK(cudaMalloc(&g->lfg, sizeof(LfgState) * cfg->pools));
     CK(cudaMalloc(&g->scratch, g->hbm ? hbm_drift_scratch_bytes(g->nvals) : sizeof(double) * 1024));
     if (g->hbm) {
-        CK(cudaMalloc(&g->gbar, kRunBarWords * sizeof(unsigned long long)));
+        CK(cudaMalloc(&g->gbar, (kRunBarWords + kRunFlowWords) * sizeof(unsigned long long)));
     }
     CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));

@@ -16,6 +16,8 @@
 // strided gather.
 #include <utility>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace wg {
@@ -1161,6 +1163,303 @@ __global__ void __launch_bounds__(kRunThreads, 2)
     if (pend_n) emit(pend_pool, pend_n, pend_off, pend_ctr);
 }
 
+// ---------------------------------------------------------------------------
+// Dataflow variant of the persistent run (WRNG_GPU_HBM_FLOW=1): the same
+// passes, rows, arithmetic and emission tiles as k_hbm_run, but no grid
+// barrier.  In the transposed storage, destination row c of pass i reads
+// exactly one storage row per array, s_m(c) = (a_m c + g_m) mod C, of pass
+// i-1's output; and the buffer row c it overwrites was read in pass i-1 by
+// exactly the rows c'_m with s_m(c'_m) = c.  So each row waits only for
+// those 8 rows of the previous pass (per-row epoch flags, release/acquire),
+// and for the emission tiles that read its buffer slot two passes earlier
+// (per 64-row group counters).  A CTA emits its tiles of an emitting pass
+// after its rows of the NEXT pass, when those tiles' rows are long done.
+// Deadlock-free: a CTA enters pass i+1 only after its rows of pass i, so the
+// least advanced CTA only waits for rows of passes every CTA has finished.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void flag_release(unsigned* f, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+__device__ __forceinline__ void flag_add_release(unsigned* f, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+__device__ __forceinline__ void flag_wait(const unsigned* f, unsigned v) {
+    unsigned x;
+    do {
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(f) : "memory");
+    } while (x < v);
+}
+// inverse of an odd a modulo 2^32 (Newton: 5 steps from 3 correct bits)
+__device__ __forceinline__ uint32_t inv_odd(uint32_t a) {
+    uint32_t x = a;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) x *= 2u - a * x;
+    return x;
+}
+
+template <typename T, int NA>
+__global__ void __launch_bounds__(kRunThreads, 2)
+    k_hbm_flow(KernelArgs a, wrng_gpu_params* params, HbmRun run, unsigned long long* gbar) {
+    extern __shared__ __align__(128) unsigned char hsm[];
+    const uint32_t N = a.N;
+    const HbmSplit sp = hbm_split(N);
+    const uint32_t R = 1u << sp.lr, C = 1u << sp.lc;
+    T* stage = reinterpret_cast<T*>(hsm);                          // [S][NA][R]
+    T(*tile)[kRunTile + 1] = reinterpret_cast<T(*)[kRunTile + 1]>(  // [64][65]
+        hsm + (size_t)kRunStages * NA * R * sizeof(T));
+    __shared__ __align__(8) uint64_t full[kRunStages];
+    __shared__ double s_c0, s_c1, s_target, s_scale, s_tracked;
+    __shared__ int s_err;
+    PoolMeta* meta = a.meta;
+    unsigned* rowflag = reinterpret_cast<unsigned*>(gbar + kRunBarWords);  // [C]: passes done
+    unsigned* emitcnt = rowflag + C;  // [ceil(C/64)]: emission tiles read, per 64-row group
+    // withheld value of each pass of the launch (a later pass of the same
+    // buffer may overwrite meta->withheld before a slow CTA has read it)
+    double* whslot = reinterpret_cast<double*>(gbar + kRunBarWords + kRunFlowRowWords);
+    const uint32_t t = threadIdx.x;
+    const bool active_t = t < R;
+    const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
+    const uint32_t full_s = (uint32_t)__cvta_generic_to_shared(full);
+    const uint32_t row_bytes = R * (uint32_t)sizeof(T);
+    const uint32_t tiles_h = (R + kRunTile - 1) / kRunTile;
+    const uint32_t tiles_per_group = tiles_h * NA;  // tiles reading one 64-row group
+    if (t == 0) {
+        for (uint32_t k = 0; k < kRunStages; ++k) mbar_init(full_s + 8 * k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s_tracked = meta->tracked[run.src0];
+    }
+    __syncthreads();
+    uint32_t q = 0;
+    // tiles of the emission of pass `ip` (pool e_pool), this CTA's share;
+    // `eidx` counts the emissions of this launch before it
+    auto emit = [&](const T* e_pool, uint64_t e_n, uint64_t e_off, uint32_t e_pass) {
+        const uint32_t tiles_l = (C + kRunTile - 1) / kRunTile;
+        const uint32_t ntiles = tiles_h * tiles_l * NA;
+        char* outc = static_cast<char*>(a.out) + e_off * (a.out_f32 ? 4 : 8);
+        const uint32_t tx = t & 31u, ty = t >> 5;
+        for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+            const uint32_t m = tl / (tiles_h * tiles_l);
+            const uint32_t rem = tl - m * tiles_h * tiles_l;
+            const uint32_t jh0 = (rem % tiles_h) * kRunTile, jl0 = (rem / tiles_h) * kRunTile;
+            const T* pool = e_pool + (uint64_t)m * N;
+            if (t < kRunTile && jl0 + t < C) {  // the tile's 64 rows of the emitted pass
+                flag_wait(rowflag + jl0 + t, e_pass + 1);
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            }
+            __syncthreads();
+            T v[8];
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k)
+#pragma unroll
+                for (uint32_t h = 0; h < 2; ++h) {
+                    const uint32_t jl = jl0 + ty + 16 * k, jh = jh0 + tx + 32 * h;
+                    v[2 * k + h] = jl < C && jh < R ? pool[(uint64_t)jl * R + jh] : (T)0;
+                }
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k)
+#pragma unroll
+                for (uint32_t h = 0; h < 2; ++h) tile[ty + 16 * k][tx + 32 * h] = v[2 * k + h];
+            __syncthreads();
+            if (t == 0) flag_add_release(emitcnt + jl0 / kRunTile, 1u);  // the tile's reads are done
+            const uint64_t mbase = (uint64_t)m * N;
+#pragma unroll
+            for (uint32_t k = 0; k < kRunTile; k += 16) {
+                const uint32_t jh = jh0 + ty + k;
+#pragma unroll
+                for (uint32_t h = 0; h < kRunTile; h += 32) {
+                    const uint32_t jl = jl0 + tx + h;
+                    const uint64_t flat = mbase + (uint64_t)jh * C + jl;
+                    if (jl < C && jh < R && flat < e_n)
+                        put_out_cs(outc, flat, tile[tx + h][ty + k], a.out_f32, a.unit,
+                                   a.mu, a.sigma);
+                }
+            }
+            __syncthreads();
+        }
+    };
+    const T* pend_pool = nullptr;  // emission owed (pass before the current one)
+    uint64_t pend_n = 0, pend_off = 0;
+    uint32_t pend_pass = 0;
+    uint32_t emissions = 0;     // emissions of this launch so far (any CTA's schedule)
+    uint32_t emit_of[2] = {0xFFFFFFFFu, 0xFFFFFFFFu};  // per buffer: index of the emission reading it
+
+    for (uint32_t i = 0; i < run.npass; ++i) {
+        const uint32_t src = run.src0 ^ (i & 1u), dst = src ^ 1u;
+        const wrng_gpu_params prm = params[run.param0 + i];
+        const wrng_gpu_params pprev = i ? params[run.param0 + i - 1] : prm;
+        const T* spool = static_cast<const T*>(a.buf[src]);
+        T* dpool = static_cast<T*>(a.buf[dst]);
+        const uint32_t nrows = blockIdx.x < C ? (C - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+        const uint32_t q0 = q;
+        // buffer dst was last read by an emission (of pass i-2): wait for its tiles
+        const uint32_t e_dst = emit_of[dst];
+        uint32_t ainv[NA];
+#pragma unroll
+        for (int m = 0; m < NA; ++m) ainv[m] = inv_odd(pprev.stride[m]);
+        // thread 0: row k's dependencies, then its sources -> stage (q0 + k) % S
+        auto issue = [&](uint32_t k) {
+            const uint32_t jlo = blockIdx.x + k * gridDim.x;
+            // RAW: the source rows of pass i-1; WAR: the pass i-1 rows that
+            // read row jlo of dst, and the emission tiles that read its group.
+            // All polled together: one round trip once they are done.
+            const unsigned* fa[2 * NA + 1];
+            unsigned ft[2 * NA + 1];
+            int nf = 0;
+            if (i > 0) {
+#pragma unroll
+                for (int m = 0; m < NA; ++m) {
+                    fa[nf] = rowflag + ((prm.stride[m] * jlo + prm.offset[m]) & (C - 1));
+                    ft[nf++] = i;
+                    fa[nf] = rowflag + ((ainv[m] * (jlo - pprev.offset[m])) & (C - 1));
+                    ft[nf++] = i;
+                }
+            }
+            if (e_dst != 0xFFFFFFFFu) {
+                fa[nf] = emitcnt + jlo / kRunTile;
+                ft[nf++] = (e_dst + 1) * tiles_per_group;
+            }
+            for (bool ok = nf == 0; !ok;) {
+                unsigned x[2 * NA + 1];
+#pragma unroll
+                for (int f = 0; f < 2 * NA + 1; ++f)
+                    if (f < nf)
+                        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];"
+                                     : "=r"(x[f])
+                                     : "l"(fa[f])
+                                     : "memory");
+                ok = true;
+#pragma unroll
+                for (int f = 0; f < 2 * NA + 1; ++f)
+                    if (f < nf) ok = ok && x[f] >= ft[f];
+            }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            const uint32_t sb = (q0 + k) % kRunStages;
+            const uint32_t bar = full_s + 8 * sb;
+            mbar_expect_tx(bar, NA * row_bytes);
+#pragma unroll
+            for (int m = 0; m < NA; ++m) {
+                const uint32_t srow = (prm.stride[m] * jlo + prm.offset[m]) & (C - 1);
+                bulk_g2s(stage_s + (sb * NA + m) * row_bytes,
+                         spool + (uint64_t)m * N + (uint64_t)srow * R, row_bytes, bar);
+            }
+        };
+        if (t == 0) {
+            int err = meta->error ? -1 : 0;
+            // the pool's withheld value comes from pass i-1's last row
+            if (i > 0) {
+                flag_wait(rowflag + (C - 1), i);
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            }
+            const double tracked = s_tracked;
+            double withheld;
+            asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];"
+                         : "=d"(withheld)
+                         : "l"(i > 0 ? &whslot[i - 1] : &meta->withheld[src])
+                         : "memory");
+            if (!err) {
+                double scale, target;
+                err = pass_scale(tracked, withheld, NA * N, a.mode, scale, target);
+                if (!err) {
+                    s_target = target;
+                    s_scale = scale;
+                    s_c0 = NA == 2 ? prm.c * scale : (prm.variant ? scale : 0.5 * scale);
+                    s_c1 = NA == 2 ? prm.s * scale : scale;
+                }
+            }
+            s_err = err;
+            if (!err)
+                for (uint32_t k = 0; k < nrows && k < kRunStages; ++k) issue(k);
+        }
+        __syncthreads();
+        if (s_err) {
+            if (pend_n) emit(pend_pool, pend_n, pend_off, pend_pass);
+            if (s_err > 0 && blockIdx.x == 0 && t == 0) meta->error = s_err;
+            return;
+        }
+        const T c0 = (T)s_c0, c1 = (T)s_c1;
+        const uint32_t variant = prm.variant;
+        for (uint32_t k = 0; k < nrows; ++k, ++q) {
+            const uint32_t jlo = blockIdx.x + k * gridDim.x;
+            const uint32_t sb = q % kRunStages;
+            mbar_wait(full_s + 8 * sb, (q / kRunStages) & 1u);
+            if (active_t) {
+                const T* rows = stage + (size_t)sb * NA * R;
+                T g[NA];
+#pragma unroll
+                for (int m = 0; m < NA; ++m) {
+                    const uint32_t sh = ((prm.stride[m] * jlo + prm.offset[m]) >> sp.lc) & (R - 1);
+                    g[m] = rows[m * R + ((prm.stride[m] * t + sh) & (R - 1))];
+                }
+                T y[NA];
+                if (NA == 2) {
+                    y[0] = c0 * g[0] + c1 * g[NA > 1 ? 1 : 0];
+                    y[NA > 1 ? 1 : 0] = c0 * g[NA > 1 ? 1 : 0] - c1 * g[0];
+                } else {
+                    const T a0 = g[0], a1 = g[NA > 1 ? 1 : 0], a2 = g[NA > 2 ? 2 : 0],
+                            a3 = g[NA > 3 ? 3 : 0];
+                    if (variant == 0) {
+                        const T pp = a0 + a1, qq = a0 - a1, rr = a2 + a3, s = a2 - a3;
+                        y[0] = c0 * (pp + rr);
+                        y[NA > 1 ? 1 : 0] = c0 * (qq + s);
+                        y[NA > 2 ? 2 : 0] = c0 * (pp - rr);
+                        y[NA > 3 ? 3 : 0] = c0 * (qq - s);
+                    } else {
+                        const T tt = (T)0.5 * ((a0 + a1) + (a2 + a3));
+                        y[0] = c0 * (tt - a0);
+                        y[NA > 1 ? 1 : 0] = c0 * (tt - a1);
+                        y[NA > 2 ? 2 : 0] = c0 * (tt - a2);
+                        y[NA > 3 ? 3 : 0] = c0 * (tt - a3);
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < NA; ++m) dpool[(uint64_t)m * N + (uint64_t)jlo * R + t] = y[m];
+                if (jlo == C - 1 && t == R - 1) {
+                    meta->withheld[dst] = (double)y[NA - 1];
+                    whslot[i] = (double)y[NA - 1];
+                }
+            }
+            __syncthreads();  // stage sb fully read, row jlo stored
+            if (t == 0) {
+                flag_release(rowflag + jlo, i + 1);  // row done: its reads and writes
+                if (k + kRunStages < nrows) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    issue(k + kRunStages);
+                }
+            }
+        }
+        // the previous emitting pass's tiles: its rows are done by now
+        if (pend_n) {
+            emit(pend_pool, pend_n, pend_off, pend_pass);
+            pend_n = 0;
+        }
+        const bool end = (run.end_mask >> i) & 1u;
+        const uint64_t emit_n = run.emit_n[i];
+        if (blockIdx.x == 0 && t == 0) {
+            params[run.param0 + i].scale = s_scale;
+            params[run.param0 + i].target_sumsq = s_target;
+            meta->tracked[dst] = s_target;
+            meta->active = dst;
+            meta->pass_count += 1;
+            meta->avail = end ? (uint64_t)NA * N - 1 - emit_n : 0;
+        }
+        if (t == 0) s_tracked = s_target;  // regenerate sets tracked = target
+        if (emit_n) {
+            pend_pool = dpool;
+            pend_n = emit_n;
+            pend_off = run.out_off[i];
+            pend_pass = i;
+            emit_of[dst] = emissions++;
+        } else {
+            emit_of[dst] = 0xFFFFFFFFu;
+        }
+        __syncthreads();
+    }
+    if (pend_n) emit(pend_pool, pend_n, pend_off, pend_pass);
+}
+
+static const bool g_hbm_flow = std::getenv("WRNG_GPU_HBM_FLOW") != nullptr;
+
 template <typename T, int NA>
 static cudaError_t hbm_run_go(const KernelArgs& a, wrng_gpu_params* params, const HbmRun& run,
                               unsigned long long* gbar, cudaStream_t st) {
@@ -1172,11 +1471,11 @@ static cudaError_t hbm_run_go(const KernelArgs& a, wrng_gpu_params* params, cons
     // cached grid size is co-resident for every pool size
     const size_t smem_max = (size_t)kRunStages * NA * 512 * sizeof(T) +
                             (size_t)kRunTile * (kRunTile + 1) * sizeof(T);
-    auto kern = k_hbm_run<T, NA>;
-    static int occ_cache[2][2][64] = {};  // [dtype][n4][device] CTAs in the grid
+    auto kern = g_hbm_flow ? k_hbm_flow<T, NA> : k_hbm_run<T, NA>;
+    static int occ_cache[2][2][2][64] = {};  // [flow][dtype][n4][device] CTAs in the grid
     int dev = 0;
     cudaGetDevice(&dev);
-    int& occ = occ_cache[sizeof(T) == 8][NA == 4][dev & 63];
+    int& occ = occ_cache[g_hbm_flow][sizeof(T) == 8][NA == 4][dev & 63];
     if (occ == 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem_max);
@@ -1191,7 +1490,9 @@ static cudaError_t hbm_run_go(const KernelArgs& a, wrng_gpu_params* params, cons
         if (occ <= 0) return cudaErrorLaunchOutOfResources;
     }
     // barrier counter + the emission tile counters of this launch
-    cudaError_t e = cudaMemsetAsync(gbar, 0, kRunBarWords * sizeof(unsigned long long), st);
+    cudaError_t e = cudaMemsetAsync(
+        gbar, 0, (kRunBarWords + (g_hbm_flow ? kRunFlowWords : 0)) * sizeof(unsigned long long),
+        st);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)occ);

@@ -137,6 +137,10 @@ constexpr uint32_t kRunMax = 64;
 // k_hbm_run's device words: grid-barrier counter, then kRunMax 32-bit
 // emission tile counters (packed two per word)
 constexpr uint32_t kRunBarWords = 1 + kRunMax / 2;
+// the dataflow run's per-row epoch flags (C <= 2048 rows) and per-64-row
+// emission counters, after the barrier words
+constexpr uint32_t kRunFlowRowWords = (2048 + 2048 / 64) / 2;
+constexpr uint32_t kRunFlowWords = kRunFlowRowWords + kRunMax;  // + per-pass withheld slots
 struct HbmRun {
     uint32_t npass, src0, param0, pad_;
     uint64_t end_mask;  // bit i: pass i ends a refill

@@ -463,7 +463,8 @@ def test_hbm_persistent_runs_match_oracle(W, n, dt, p, f, drift, restart):
 
 
 def test_hbm_run_and_stepwise_paths_agree(W):
-    """WRNG_GPU_HBM_STEPWISE=1 (one launch per pass and per emission) and the
+    """WRNG_GPU_HBM_STEPWISE=1 (one launch per pass and per emission),
+    WRNG_GPU_HBM_FLOW=1 (row-level dataflow, no grid barrier) and the
     default persistent runs give the same bits (subprocess: the switch is
     read when the library loads)."""
     import subprocess
@@ -482,12 +483,12 @@ def test_hbm_run_and_stepwise_paths_agree(W):
         "print(h.hexdigest())\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for env in ({}, {"WRNG_GPU_HBM_STEPWISE": "1"}):
+    for env in ({}, {"WRNG_GPU_HBM_STEPWISE": "1"}, {"WRNG_GPU_HBM_FLOW": "1"}):
         r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, **env),
                            capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stderr
         outs.append(r.stdout.strip().splitlines()[-1])
-    assert outs[0] == outs[1]
+    assert outs[0] == outs[1] == outs[2]
 
 
 def test_hbm_run_small_then_large_pool_in_one_process(W):
