@@ -607,10 +607,6 @@ wrng_gpu_status run_hbm(wrng_gpu* g, uint32_t p, Ctr c, const std::vector<Ev>& e
                 c.active ^= 1u;
                 if (e.emit_n)
                     LAUNCH(launch_hbm_emit_t(NA, dt, a, c.active, e.emit_n, e.out_off, s));
-            } else if (e.kind == Ev::DRIFT) {
-                LAUNCH(launch_hbm_drift(NA, dt, a, c.active,
-                                        (g->cfg.flags & WRNG_GPU_DRIFT_TREE) != 0, g->scratch,
-                                        s));
             }
         }
         if (jend < ev.size() && ev[jend].kind == Ev::DRIFT) {

@@ -767,6 +767,36 @@ def test_uniform_state_write_back(W, force_hbm):
         a.set_uniform_state(bad)
 
 
+@pytest.mark.parametrize("n,dt,p", [(2, "f64", 10), (4, "f32", 8), (4, "f64", 11)])
+def test_small_host_fills_bit_exact(W, n, dt, p):
+    """Host fills of at most one refill's worth are served from the host
+    window (capi.cu fill_window): random sizes, mu/sigma and output widths,
+    interleaved with device-path fills, advance_pass, refill and a save/load
+    round trip — every value and counter as the oracle's."""
+    kw = dict(pool_exponent=p, throwaway_f=2, seed=41, n_arrays=n, dtype=dt, drift_check_period=5,
+              restart_interval_passes=9)
+    g = gpu_state(W, **kw)
+    o = oracle_state(**kw)
+    cap = n * (1 << p) - 1
+    rng = np.random.default_rng(p)
+    for it in range(60):
+        cnt = int(rng.integers(0, cap + 1)) if it % 7 else int(rng.integers(cap, 3 * cap))
+        mu, sigma = (0.0, 1.0) if it % 3 else (float(rng.normal()), float(rng.uniform(0, 3)))
+        od = ("f64", np.float64) if it % 2 else ("f32", np.float32)
+        assert_bits(g.fill(cnt, mu, sigma, dtype=od[0]), o.fill(cnt, mu, sigma, out_dtype=od[1]))
+        if it % 11 == 5:
+            g.advance_pass()
+            o.advance_pass()
+        if it % 13 == 7:
+            g.refill()
+            o.refill()
+        if it == 30:
+            g = W.WallaceState.load_state(g.save_state())
+        oc = o.counters()
+        assert (g.pass_count(), g.numbers_emitted(), g.avail()) == (
+            oc["pass_count"], oc["numbers_emitted"], oc["avail"])
+
+
 def test_zero_tracked_sum_raises(W):
     g = gpu_state(W, pool_exponent=10, seed=3)
     p = g.active_pool()
