@@ -54,6 +54,9 @@ const uint32_t g_bulk_align = bulk_align_bytes();
 // random DSMEM gathers are request-bound, slower than one CTA for C1;
 // DESIGN.md §5).
 const bool g_cluster = std::getenv("WRNG_GPU_CLUSTER") != nullptr;
+// Small n = 4 pools (4x256, fp32 4x512) fill on the group engine, several
+// pools per warp; WRNG_GPU_NO_GROUP=1 keeps them on one CTA per pool (A/B).
+const bool g_group = std::getenv("WRNG_GPU_NO_GROUP") == nullptr;
 // HBM engine: consecutive passes run as one persistent launch (k_hbm_run);
 // WRNG_GPU_HBM_STEPWISE=1 launches one kernel per pass and per emission.
 const bool g_hbm_run = std::getenv("WRNG_GPU_HBM_STEPWISE") == nullptr;
@@ -474,6 +477,16 @@ void plan_fill(const wrng_gpu* g, Ctr& c, uint64_t len, std::vector<Ev>* ev) {
         done = take;
         c.avail -= take;
     }
+    if (!ev && R == 0 && done < len) {
+        // no event list and no restarts: the counters in closed form (a bank
+        // fill plans thousands of pools x thousands of refills per call)
+        const uint64_t rem = len - done, nref = (rem + cap - 1) / cap;
+        c.pc += nref * f;
+        c.active ^= (uint32_t)((nref * f) & 1u);
+        c.avail = cap - (rem - (nref - 1) * cap);
+        c.emitted += len;
+        return;
+    }
     while (done < len) {
         const uint64_t before = c.pc;
         const bool will_restart = R > 0 && crossed(before, before + f, R);
@@ -656,9 +669,14 @@ wrng_gpu_status fill_device(wrng_gpu* g, void* out, int out_f32, const OutLayout
                           : 0u;
         a.host_restart = host_bm(g) && g->cfg.restart_interval_passes > 0;
         a.stats = stats;
+        const bool unit_same = unit && (out_f32 != 0) == (g->cfg.dtype == WRNG_GPU_F32);
         if (g_cluster && !stats && g->cfg.restart_interval_passes == 0 &&
             cluster_engine_fits(g->cfg.n_arrays, g->cfg.dtype, g->N, P))
             LAUNCH(launch_cluster(g->cfg.n_arrays, g->cfg.dtype, a, s));
+        else if (g_group && !stats && unit_same && a.bulk_emit &&
+                 g->cfg.restart_interval_passes == 0 &&
+                 group_engine_fits(g->cfg.n_arrays, g->cfg.dtype, g->N))
+            LAUNCH(launch_group(g->cfg.dtype, a, s));
         else
             LAUNCH(launch_smem(g->cfg.n_arrays, g->cfg.dtype, a, s));
         if (a.host_restart) {
@@ -1591,7 +1609,10 @@ int64_t wrng_gpu_resident_pools(const wrng_gpu_config* cfg) {
     a.N = N;
     a.f = cfg->throwaway_f;
     a.out = &per_sm;
-    if (launch_smem(cfg->n_arrays, cfg->dtype, a, nullptr) != cudaSuccess ||
+    const bool grp = g_group && cfg->restart_interval_passes == 0 &&
+                     group_engine_fits(cfg->n_arrays, cfg->dtype, N);
+    if ((grp ? launch_group(cfg->dtype, a, nullptr)
+             : launch_smem(cfg->n_arrays, cfg->dtype, a, nullptr)) != cudaSuccess ||
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device) != cudaSuccess)
         return -(int64_t)WRNG_GPU_ECUDA;
     return (int64_t)per_sm * sms;

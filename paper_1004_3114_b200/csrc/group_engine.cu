@@ -1,0 +1,646 @@
+// Group engine: SEVERAL small pools per warp (BASELINE.json configs[4], the
+// 4x256 shapes).  A 4x256 pool gives one warp only 8 columns per thread, so
+// in the one-CTA-per-pool engine (smem_impl.cuh) two thirds of a pass's
+// instructions are its per-pass scalar work (parameter draw, fp64 chi-squared
+// scale, emission bookkeeping).  Here a pool belongs to a GROUP of G = N / J
+// lanes (J = 32 fp32 / 16 fp64 columns per lane, as in C3), a warp carries
+// 32 / G pools side by side, and every lane runs its own pool's scalar work:
+// the fixed cost of a pass is paid once per warp for 4 (fp32) or 2 (fp64)
+// pools.  Groups synchronise with __syncwarp(group mask) only and never
+// depend on one another, so a group whose control flow differs (another
+// matrix variant, an error, one refill more) just diverges for that stretch.
+//
+// Same algorithm, state and results as k_smem (bit-identical, tested):
+//   pass            wallace.cpp:113-137 in the modular form (a*j + g) & (N-1)
+//   parameters      wallace.cpp:54-58 / docs/n4_spec.md §2 (9 words per pass)
+//   scale           wallace.cpp:59-69
+//   refill / fill   wallace.cpp:188-216
+//   drift audit     wallace.cpp:225-234 with Pool::direct_sumsq (13-18)
+// Differences in mechanism only:
+//   * the lag table stays in global memory (LfgState::table, L2-resident):
+//     a group produces the words of up to 28 passes at a time — the step
+//     x[i] += x[i+334] is hazard-free for up to 273 consecutive words
+//     (common.cuh) — into a 2 KiB shared word buffer; words a failing pass
+//     leaves unconsumed are un-drawn (x[i] -= x[i+334]), so the generator
+//     state after an error is the reference's;
+//   * the drift audit of a 1024-term pool is the plain sequential loop on
+//     lane 0 of each group (all groups of a warp audit on the same pass);
+//   * full refills leave through the bulk-copy engine from a rotated pool,
+//     16/64-byte aligned spans, exactly as in smem_impl.cuh.
+// Thread-to-column map: register slot k of lane l holds column
+// j = (k*G + l) mod N (l the lane in the WARP, not in the group), so in every
+// phase C store instruction the 32 lanes of the warp write 32 different banks
+// although the pools sit 4 or 8 KiB apart (with j = k*G + lane-in-group the
+// groups collided 4-way).  Only the last PPW slots can wrap.
+// Fills only (unit output of the pool's dtype, no restarts); every other
+// operation on such a handle runs on k_smem over the same device state.
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace wg {
+namespace grp {
+
+extern __shared__ __align__(16) unsigned char g_gsm[];
+
+constexpr uint32_t kWPass = 28;                // passes per word batch
+constexpr uint32_t kWWords = kWPass * 9;       // 252 <= 273: hazard-free step
+constexpr uint32_t kWBytes = 2048;             // word buffer per pool
+static_assert(kWWords * 8 <= kWBytes && kWWords <= kShortLag, "word batch");
+
+template <typename T, int LOGN>
+struct Shape {
+    static constexpr uint32_t N = 1u << LOGN;
+    static constexpr uint32_t ES = (uint32_t)sizeof(T);
+    static constexpr uint32_t J = ES == 4 ? 32 : 16;  // columns per lane: 128 data registers
+    static constexpr uint32_t G = N / J;              // lanes per pool
+    static constexpr uint32_t PPW = 32 / G;           // pools per warp
+    static_assert(G >= 8 && G <= 16, "group engine shapes: 2 or 4 pools per warp");
+    static constexpr uint32_t ABYTES = N * ES;
+    static constexpr uint32_t PBYTES = 4 * ABYTES;
+    static constexpr uint32_t MASK = N - 1;
+    static constexpr uint32_t MASKB = MASK * ES;
+    static constexpr uint32_t NVALS = 4 * N;
+    static constexpr uint32_t CAP = NVALS - 1;
+    static constexpr uint32_t VEC = 16 / ES;
+    // fp32 pools are interleaved element by element (PoolView below)
+    static constexpr bool IL = ES == 4;
+    // shared layout: word buffers | (pad to an aligned address) | pools
+    static constexpr uint32_t BYTES = PPW * kWBytes + (IL ? PPW : 1) * ABYTES + PPW * PBYTES;
+};
+
+template <int B, int E, typename F>
+__device__ __forceinline__ void sfor(F&& f) {
+    if constexpr (B < E) {
+        f(std::integral_constant<int, B>{});
+        sfor<B + 1, E>(f);
+    }
+}
+
+template <typename T, uint32_t OFF>
+__device__ __forceinline__ T lds(uint32_t a) {
+    T v;
+    if constexpr (sizeof(T) == 4)
+        asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"(OFF));
+    else
+        asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(OFF));
+    return v;
+}
+template <typename T, uint32_t OFF>
+__device__ __forceinline__ void sts(uint32_t a, T v) {
+    if constexpr (sizeof(T) == 4)
+        asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(a), "n"(OFF), "f"(v) : "memory");
+    else
+        asm volatile("st.shared.f64 [%0+%1], %2;" ::"r"(a), "n"(OFF), "d"(v) : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(uint64_t dst, uint32_t src_s, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(src_s), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Packed fp32 (Blackwell add/sub/mul.rn.f32x2: each half rounds like the
+// scalar operation).
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2_pack(float a, float b) {
+    f2_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(f2_t v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+    f2_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t f2_sub(f2_t a, f2_t b) {
+    f2_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
+    f2_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+// One thread's columns of a pass: fp32 as packed pairs of columns (2kp, 2kp+1).
+template <typename T, uint32_t J>
+struct Cols {
+    T v[4][J];
+};
+template <uint32_t J>
+struct Cols<float, J> {
+    f2_t v[4][J / 2];
+};
+
+// Unscaled n = 4 transform in place (docs/n4_spec.md §3; operation order of
+// smem_impl.cuh's transform_b / transform_b2).
+template <typename T, uint32_t J>
+__device__ __forceinline__ void transform(Cols<T, J>& u, uint32_t variant) {
+    if constexpr (sizeof(T) == 4) {
+        if (variant == 0) {
+            sfor<0, (int)J / 2>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                const f2_t G0 = u.v[0][k], G1 = u.v[1][k], G2 = u.v[2][k], G3 = u.v[3][k];
+                const f2_t PP = f2_add(G0, G1), Q = f2_sub(G0, G1);
+                const f2_t R = f2_add(G2, G3), Sd = f2_sub(G2, G3);
+                u.v[0][k] = f2_add(PP, R);
+                u.v[1][k] = f2_add(Q, Sd);
+                u.v[2][k] = f2_sub(PP, R);
+                u.v[3][k] = f2_sub(Q, Sd);
+            });
+        } else {
+            const f2_t H = f2_pack(0.5f, 0.5f);
+            sfor<0, (int)J / 2>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                const f2_t G0 = u.v[0][k], G1 = u.v[1][k], G2 = u.v[2][k], G3 = u.v[3][k];
+                const f2_t Tt = f2_mul(H, f2_add(f2_add(G0, G1), f2_add(G2, G3)));
+                u.v[0][k] = f2_sub(Tt, G0);
+                u.v[1][k] = f2_sub(Tt, G1);
+                u.v[2][k] = f2_sub(Tt, G2);
+                u.v[3][k] = f2_sub(Tt, G3);
+            });
+        }
+    } else {
+        if (variant == 0) {
+            sfor<0, (int)J>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                const T g0 = u.v[0][k], g1 = u.v[1][k], g2 = u.v[2][k], g3 = u.v[3][k];
+                const T pp = g0 + g1, q = g0 - g1, r = g2 + g3, s = g2 - g3;
+                u.v[0][k] = pp + r;
+                u.v[1][k] = q + s;
+                u.v[2][k] = pp - r;
+                u.v[3][k] = q - s;
+            });
+        } else {
+            sfor<0, (int)J>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                const T g0 = u.v[0][k], g1 = u.v[1][k], g2 = u.v[2][k], g3 = u.v[3][k];
+                const T t = (T)0.5 * ((g0 + g1) + (g2 + g3));
+                u.v[0][k] = t - g0;
+                u.v[1][k] = t - g1;
+                u.v[2][k] = t - g2;
+                u.v[3][k] = t - g3;
+            });
+        }
+    }
+}
+
+// Phase C bookkeeping of a bulk-emitting pass (smem_impl.cuh's PhaseC with
+// the group for the CTA).
+struct PhaseC {
+    uint32_t my_s;
+    uint32_t j0, jend, jend_last;
+    uint32_t src0;
+};
+
+// A group's pool in shared memory, natural flat index i = m*N + j:
+//   IL (fp32): the PPW pools of the warp interleaved element by element —
+//     pool q's value i at word i*PPW + q — so the bank of an access is
+//     (PPW*i + q) mod 32: the G lanes of a group (consecutive or odd-stride
+//     j) hit G distinct banks congruent to q mod PPW, and no two groups of
+//     the warp ever share a bank: gathers and stores are conflict-free by
+//     construction (separate pools: 3.1 wavefronts per gather, ncu);
+//   else (fp64: a group is a half-warp, which 64-bit accesses serve
+//     separately): contiguous, each array rotated by rot (bulk emission).
+template <typename T, bool IL, uint32_t PPW, uint32_t MASK>
+struct PoolView {
+    const T* p;  // IL: warp's pool block + q; else the group's pool
+    uint32_t rot;
+    __device__ __forceinline__ T operator[](uint32_t i) const {
+        if constexpr (IL)
+            return p[i * PPW];
+        else
+            return p[(i & ~MASK) | ((i + rot) & MASK)];
+    }
+};
+
+template <typename T, int LOGN>
+__global__ void __launch_bounds__(32, 8) k_group(const KernelArgs a) {
+    using S = Shape<T, LOGN>;
+    constexpr uint32_t N = S::N, G = S::G, J = S::J, ES = S::ES, VEC = S::VEC, PPW = S::PPW;
+    constexpr bool IL = S::IL;
+    constexpr uint64_t CAP = S::CAP;
+    // element stride and array stride of a pool in shared memory (bytes)
+    constexpr uint32_t EST = IL ? PPW * ES : ES;
+    constexpr uint32_t AST = N * EST;
+    constexpr uint32_t MASKE = (N - 1) * EST;
+    const uint32_t lane = threadIdx.x;
+    const uint32_t q = lane / G, gl = lane % G;
+    const uint32_t gmask = ((1u << G) - 1u) << (q * G);
+    const uint32_t p = blockIdx.x * PPW + q;
+    if (p >= a.pools) return;  // the other groups never wait for this one
+    PoolMeta* meta = a.meta + p;
+    LfgState* lg = a.lfg + p;
+    // a device-raised error is sticky until the host observes it
+    if (meta->error) return;
+
+    const uint32_t base_s = (uint32_t)__cvta_generic_to_shared(g_gsm);
+    uint64_t* wbuf = reinterpret_cast<uint64_t*>(g_gsm + q * kWBytes);
+    // pools start on an AST-aligned shared address: a gather address is
+    // (index & mask) | base plus an immediate array offset
+    const uint32_t pool0_s = (base_s + PPW * kWBytes + AST - 1) / AST * AST;
+    const uint32_t pool_s = IL ? pool0_s + q * ES : pool0_s + q * S::PBYTES;
+    T* const pool = reinterpret_cast<T*>(g_gsm + (pool_s - base_s));
+    uint64_t* tab = lg->table;
+    // this lane's slot-0 column: IL: j = k*G + gl; else j = (k*G + lane) mod N,
+    // so the 32 lanes of a store hit 32 banks although the pools sit 8 KiB apart
+    const uint32_t jl = IL ? gl : lane;
+
+    // ---- load state -------------------------------------------------------
+    uint64_t pc = meta->pass_count, avail = meta->avail, emitted = meta->emitted;
+    uint32_t act = meta->active;
+    double tracked = meta->tracked[act], withheld = meta->withheld[act];
+    double prev_tracked = 0.0, prev_withheld = 0.0;
+    bool have_prev = false;
+    uint32_t r = lg->r;         // cursor at the start of the current word batch
+    uint64_t draws = lg->draws;
+    {
+        const T* srcp = static_cast<const T*>(a.buf[act]) + (uint64_t)p * S::NVALS;
+        if constexpr (IL) {
+            for (uint32_t i = gl; i < S::NVALS; i += G) pool[i * PPW] = srcp[i];
+        } else {
+            const uint4* src = reinterpret_cast<const uint4*>(srcp);
+            uint4* dst = reinterpret_cast<uint4*>(pool);
+            constexpr uint32_t NVEC = S::NVALS * ES / 16;
+            for (uint32_t i = gl; i < NVEC; i += G) dst[i] = src[i];
+        }
+    }
+    __syncwarp(gmask);
+
+    const uint64_t len = a.lay.len_base + (p < a.lay.len_extra ? 1 : 0);
+    const uint64_t out_base =
+        (uint64_t)p * a.lay.off_stride + (p < a.lay.off_extra ? p : a.lay.off_extra);
+    T* const outv = static_cast<T*>(a.out) + out_base;
+    const uint32_t f = a.f, mode = a.mode;
+    // bulk span alignment in elements: the ragged head (< bvec) stays inside
+    // column group 0, the tail (<= bvec + VEC - 2) inside the last one
+    uint32_t bvec = VEC;
+    if constexpr (!IL) {
+        const uint32_t want = a.bulk_emit / ES;
+        while (bvec * 2 <= want && bvec * 2 <= G && bvec * 2 + VEC <= G + 2) bvec *= 2;
+    }
+    PeriodCounter drift;
+    drift.init(a.drift, pc);
+
+    uint64_t done = 0;
+    if (avail > 0 && len > 0) {
+        // leftover of the live pool: flat [pos, pos + take)
+        const uint64_t take = umin64(len, avail);
+        const uint32_t pos = (uint32_t)(CAP - avail);
+        const PoolView<T, IL, PPW, S::MASK> v{pool, 0u};
+        for (uint32_t i = gl; i < (uint32_t)take; i += G) outv[i] = v[pos + i] + (T)0;
+        done = take;
+        avail -= take;
+    }
+    const uint64_t total_passes = (len - done + CAP - 1) / CAP * f;
+    uint64_t pass_i = 0;
+    uint32_t rot = 0;    // !IL: value j of each array sits at (j + rot) mod N
+    uint32_t wleft = 0;  // passes whose words are still in wbuf
+    uint32_t wpos = 0;   // next word in wbuf
+    uint32_t wcnt = 0;   // words of the current batch
+    int err = 0;
+    bool bulk_pending = false;
+
+    while (!err && done < len) {
+        // refill (wallace.cpp:188-196), the exposed window fused into its last pass
+        const bool will_drift = drift.will_cross(f);
+        const uint32_t emit_n = (uint32_t)umin64(len - done, CAP);
+        T* const out_p = outv + done;
+        for (uint32_t i = 0; i < f; ++i) {
+            if (wleft == 0) {
+                // next batch of uniform words, straight from the global lag table
+                const uint64_t left = total_passes - pass_i;
+                r += wcnt;
+                r = r >= kTable ? r - kTable : r;
+                wleft = left < kWPass ? (uint32_t)left : kWPass;
+                wcnt = wleft * 9;
+                wpos = 0;
+#pragma unroll 4
+                for (uint32_t k = gl; k < wcnt; k += G) {
+                    uint32_t ii = r + k;
+                    ii = ii >= kTable ? ii - kTable : ii;
+                    uint32_t ss = ii + kGap;
+                    ss = ss >= kTable ? ss - kTable : ss;
+                    const uint64_t w = __ldcg(tab + ii) + __ldcg(tab + ss);
+                    __stcg(tab + ii, w);
+                    wbuf[k] = w;
+                }
+                __syncwarp(gmask);
+            }
+            ++pass_i;
+            const bool last_launch = pass_i == total_passes;
+            const uint32_t en = i + 1 == f ? emit_n : 0u;
+
+            // ---- this pass's parameters (docs/n4_spec.md §2) --------------
+            uint32_t ixb[4], stepb[4];
+            uint32_t variant;
+            {
+                const uint64_t* w = wbuf + wpos;
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const uint32_t lo = m == 0 ? 3u : m == 1 ? 7u : m == 2 ? 13u : 19u;
+                    const uint32_t st = (w[m] >> 63) ? lo + (m == 0 ? 2u : 4u) : lo;
+                    const uint32_t off = (uint32_t)(w[4 + m] >> (64 - LOGN));
+                    ixb[m] = (st * jl + off + rot) * EST;
+                    stepb[m] = st * G * EST;
+                }
+                variant = (uint32_t)(w[8] >> 63);
+            }
+            wpos += 9;
+            --wleft;
+            draws += 9;
+            double scale = 0.0, target = 0.0;
+            if (pass_scale(tracked, withheld, S::NVALS, mode, scale, target)) {
+                err = WRNG_GPU_ECORRUPT;  // wallace.cpp:59-61, after the draws
+                break;
+            }
+            // regenerate folds the scale into the matrix (wallace.cpp:116-117)
+            const T c0 = (T)(variant ? scale : 0.5 * scale);
+            if (last_launch) {
+                // the pre-pass pool becomes the inactive buffer (wallace.cpp:170-174)
+                T* prev = static_cast<T*>(a.buf[act]) + (uint64_t)p * S::NVALS;
+                const PoolView<T, IL, PPW, S::MASK> v{pool, rot};
+                for (uint32_t k = gl; k < S::NVALS; k += G) prev[k] = v[k];
+                prev_tracked = tracked;
+                prev_withheld = withheld;
+                have_prev = true;
+            }
+            // emission mode: 0 none, 2 warp stores of the window [0, en),
+            // 3 (contiguous pools) full refill through the bulk-copy engine
+            // (1: interleaved pools, full refill through warp stores)
+            const uint32_t md = en == 0 ? 0u : en == (uint32_t)CAP ? (IL ? 1u : 3u) : 2u;
+            // new rotation: on a bulk-emitting pass, the output's 16-byte phase
+            const uint32_t ophase = (uint32_t)(reinterpret_cast<uintptr_t>(out_p) / ES);
+            const uint32_t rot2 = md == 3 ? ophase & (VEC - 1) : rot;
+            PhaseC c;
+            c.my_s = pool_s + (jl + rot2) * EST;
+            // !IL: the last PPW slots can wrap: their columns and shared addresses
+            uint32_t wj[PPW], wa[PPW];
+            if constexpr (!IL) {
+#pragma unroll
+                for (uint32_t i2 = 0; i2 < PPW; ++i2) {
+                    wj[i2] = ((J - PPW + i2) * G + lane) & S::MASK;
+                    wa[i2] = (((wj[i2] + rot2) * ES) & S::MASKB) | pool_s;
+                }
+                const uint32_t ph = ophase & (bvec - 1);
+                c.j0 = (bvec - ph) & (bvec - 1);
+                c.jend = c.j0 + ((N - rot2 - c.j0) & ~(bvec - 1));
+                c.jend_last = c.j0 + ((umin32(N - rot2, N - 1) - c.j0) & ~(bvec - 1));
+                c.src0 = pool_s + (c.j0 + rot2) * ES;
+            }
+
+            // ---- phase B: gather every column, then the transform ---------
+            Cols<T, J> u;
+            if constexpr (ES == 4) {
+                sfor<0, (int)J / 2>([&](auto kc) {
+                    constexpr int kp = decltype(kc)::value;
+                    float g[4][2];
+                    sfor<0, 2>([&](auto hc) {
+                        constexpr int h = decltype(hc)::value;
+                        sfor<0, 4>([&](auto mc) {
+                            constexpr int m = decltype(mc)::value;
+                            g[m][h] = lds<float, (uint32_t)m * AST>((ixb[m] & MASKE) | pool_s);
+                            ixb[m] += stepb[m];
+                        });
+                    });
+                    sfor<0, 4>([&](auto mc) {
+                        constexpr int m = decltype(mc)::value;
+                        u.v[m][kp] = f2_pack(g[m][0], g[m][1]);
+                    });
+                });
+            } else {
+                sfor<0, (int)J>([&](auto kc) {
+                    constexpr int k = decltype(kc)::value;
+                    sfor<0, 4>([&](auto mc) {
+                        constexpr int m = decltype(mc)::value;
+                        u.v[m][k] = lds<T, (uint32_t)m * AST>((ixb[m] & MASKE) | pool_s);
+                        ixb[m] += stepb[m];
+                    });
+                });
+            }
+            transform<T, J>(u, variant);
+            // phase C rewrites the pool: the group's gathers are done, and the
+            // previous refill's bulk copies have read it
+            if (bulk_pending && gl == 0) bulk_wait_read();
+            __syncwarp(gmask);
+
+            // ---- phase C: scale, store in place, emit ---------------------
+            double wh = 0.0;
+            T* const ob = out_p + jl;
+            // one instantiation per emission mode MD
+            auto phase_c = [&](auto mdc) {
+                constexpr uint32_t MD = decltype(mdc)::value;
+                auto put = [&](auto mc, auto kc, T y) {
+                    constexpr int m = decltype(mc)::value;
+                    constexpr int k = decltype(kc)::value;
+                    // emitted form 0 + 1 * v (-0.0 -> +0.0); on MD 3 the pool
+                    // holds it, being the bulk source
+                    const T e = MD == 0 ? y : y + (T)0;
+                    const T sv = MD == 3 ? e : y;
+                    if constexpr (IL || k < (int)(J - PPW)) {
+                        constexpr uint32_t col = (uint32_t)m * N + (uint32_t)k * G;
+                        sts<T, (uint32_t)m * AST + (uint32_t)k * G * EST>(c.my_s, sv);
+                        if constexpr (MD == 3 && k == 0) {  // ragged head (group 0's lanes)
+                            if (lane < c.j0) ob[col] = e;
+                        }
+                        if constexpr (MD == 2) {
+                            if (col + jl < en) ob[col] = e;
+                        }
+                        if constexpr (MD == 1) {  // everything but the withheld value
+                            if (!(m == 3 && k == (int)J - 1) || jl != G - 1) ob[col] = e;
+                        }
+                        if constexpr (IL && m == 3 && k == (int)J - 1) wh = (double)y;
+                    } else {
+                        constexpr int i2 = k - (int)(J - PPW);
+                        const uint32_t j = wj[i2];
+                        sts<T, (uint32_t)m * AST>(wa[i2], sv);
+                        if constexpr (MD == 3) {  // ragged head (column 0), tail (last column)
+                            const bool own =
+                                j < c.j0 ||
+                                (m == 3 ? (j >= c.jend_last && j != N - 1) : j >= c.jend);
+                            if (own) out_p[(uint32_t)m * N + j] = e;
+                        }
+                        if constexpr (MD == 2) {
+                            if ((uint32_t)m * N + j < en) out_p[(uint32_t)m * N + j] = e;
+                        }
+                        if constexpr (m == 3) {
+                            if (j == N - 1) wh = (double)y;
+                        }
+                    }
+                };
+                if constexpr (ES == 4) {
+                    const f2_t C = f2_pack(c0, c0);
+                    sfor<0, (int)J / 2>([&](auto kc) {
+                        constexpr int kp = decltype(kc)::value;
+                        sfor<0, 4>([&](auto mc) {
+                            constexpr int m = decltype(mc)::value;
+                            float y0, y1;
+                            f2_unpack(f2_mul(C, u.v[m][kp]), y0, y1);
+                            put(mc, std::integral_constant<int, 2 * kp>{}, y0);
+                            put(mc, std::integral_constant<int, 2 * kp + 1>{}, y1);
+                        });
+                    });
+                } else {
+                    sfor<0, (int)J>([&](auto kc) {
+                        constexpr int k = decltype(kc)::value;
+                        sfor<0, 4>([&](auto mc) {
+                            constexpr int m = decltype(mc)::value;
+                            put(mc, kc, c0 * u.v[m][k]);
+                        });
+                    });
+                }
+            };
+            if (md == 0)
+                phase_c(std::integral_constant<uint32_t, 0>{});
+            else if (!IL && md == 3)
+                phase_c(std::integral_constant<uint32_t, 3>{});
+            else if (IL && md == 1)
+                phase_c(std::integral_constant<uint32_t, 1>{});
+            else
+                phase_c(std::integral_constant<uint32_t, 2>{});
+            if (md == 3) fence_async_smem();  // generic -> async proxy
+            tracked = target;                                  // wallace.cpp:135
+            withheld = __shfl_sync(gmask, wh, G - 1, G);       // wallace.cpp:136
+            act ^= 1u;
+            rot = rot2;
+            ++pc;
+            __syncwarp(gmask);
+            if (md == 3) {
+                if (gl == 0) {
+                    // [j0, jend) of every array (last: jend_last) -> output
+                    const uint64_t o = reinterpret_cast<uint64_t>(out_p);
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        const uint32_t je = m == 3 ? c.jend_last : c.jend;
+                        if (je > c.j0)
+                            bulk_store(o + ((uint64_t)m * N + c.j0) * ES,
+                                       c.src0 + (uint32_t)m * S::ABYTES, (je - c.j0) * ES);
+                    }
+                    bulk_commit();
+                }
+                bulk_pending = true;
+            }
+        }
+        if (err) break;
+        drift.advance(f);
+        avail = CAP;
+        if (will_drift) {
+            // wallace.cpp:225-234 with Pool::direct_sumsq order (wallace.cpp:13-18)
+            double rec = 0.0;
+            if (gl == 0) {
+                const PoolView<T, IL, PPW, S::MASK> v{pool, rot};
+#pragma unroll 8
+                for (uint32_t k = 0; k < S::NVALS; ++k) {
+                    const double d = (double)v[k];
+                    rec = rec + d * d;
+                }
+            }
+            rec = __shfl_sync(gmask, rec, 0, G);
+            const double rel = fabs(rec / tracked - 1.0);
+            if (!(rel <= 1e-3)) {
+                err = WRNG_GPU_ECORRUPT;
+                break;
+            }
+            tracked = rec;
+        }
+        done += emit_n;
+        avail -= emit_n;
+    }
+    if (!err) emitted += len;
+
+    // ---- write back -------------------------------------------------------
+    if (bulk_pending && gl == 0) bulk_wait_all();  // bulk copies complete before exit
+    // words drawn ahead of a failing pass are un-drawn (x[i] -= x[i+334]; the
+    // slots a batch reads are not written by it)
+    for (uint32_t k = wpos + gl; k < wcnt; k += G) {
+        uint32_t ii = r + k;
+        ii = ii >= kTable ? ii - kTable : ii;
+        uint32_t ss = ii + kGap;
+        ss = ss >= kTable ? ss - kTable : ss;
+        __stcg(tab + ii, __ldcg(tab + ii) - __ldcg(tab + ss));
+    }
+    r += wpos;
+    r = r >= kTable ? r - kTable : r;
+    __syncwarp(gmask);
+    if (pass_i > 0) {
+        T* dst = static_cast<T*>(a.buf[act]) + (uint64_t)p * S::NVALS;
+        if (!IL && rot == 0) {
+            constexpr uint32_t NVEC = S::NVALS * ES / 16;
+            for (uint32_t i = gl; i < NVEC; i += G)
+                reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(pool)[i];
+        } else {  // back to natural order
+            const PoolView<T, IL, PPW, S::MASK> v{pool, rot};
+            for (uint32_t i = gl; i < S::NVALS; i += G) dst[i] = v[i];
+        }
+    }
+    if (gl == 0) {
+        lg->r = r;
+        lg->draws = draws;
+        meta->tracked[act] = tracked;
+        meta->withheld[act] = withheld;
+        if (have_prev) {
+            meta->tracked[act ^ 1u] = prev_tracked;
+            meta->withheld[act ^ 1u] = prev_withheld;
+        }
+        meta->active = act;
+        meta->pass_count = pc;
+        meta->avail = avail;
+        meta->emitted = emitted;
+        meta->error = (uint32_t)err;
+        meta->restart_pending = 0u;
+        meta->fill_done = done;
+    }
+}
+
+template <typename T, int LOGN>
+static cudaError_t go(const KernelArgs& a, cudaStream_t st) {
+    using S = Shape<T, LOGN>;
+    auto kern = k_group<T, LOGN>;
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
+    if (e != cudaSuccess) return e;
+    if (a.op == OP_QUERY) {  // pools per SM
+        int ctas = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, kern, 32, S::BYTES);
+        *static_cast<int*>(a.out) = ctas * (int)S::PPW;
+        return e;
+    }
+    kern<<<(a.pools + S::PPW - 1) / S::PPW, 32, S::BYTES, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace grp
+
+bool group_engine_fits(uint32_t n_arrays, uint32_t dtype, uint32_t N) {
+    if (n_arrays != 4) return false;
+    return dtype == WRNG_GPU_F64 ? N == 256 : (N == 256 || N == 512);
+}
+
+cudaError_t launch_group(uint32_t dtype, const KernelArgs& a, cudaStream_t st) {
+    if (dtype == WRNG_GPU_F64) {
+        if (a.N == 256) return grp::go<double, 8>(a, st);
+    } else {
+        if (a.N == 256) return grp::go<float, 8>(a, st);
+        if (a.N == 512) return grp::go<float, 9>(a, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace wg
