@@ -675,7 +675,9 @@ wrng_gpu_status fill_device(wrng_gpu* g, void* out, int out_f32, const OutLayout
             LAUNCH(launch_cluster(g->cfg.n_arrays, g->cfg.dtype, a, s));
         else if (g_group && !stats && unit_same && a.bulk_emit &&
                  g->cfg.restart_interval_passes == 0 &&
-                 group_engine_fits(g->cfg.n_arrays, g->cfg.dtype, g->N))
+                 group_engine_fits(g->cfg.n_arrays, g->cfg.dtype, g->N) &&
+                 // its loop counters are 32-bit: passes per pool in this call
+                 ((lay.len_base + 1) / g->cap + 2) * g->cfg.throwaway_f < (1ull << 31))
             LAUNCH(launch_group(g->cfg.dtype, a, s));
         else
             LAUNCH(launch_smem(g->cfg.n_arrays, g->cfg.dtype, a, s));

@@ -27,11 +27,12 @@
 //     lane 0 of each group (all groups of a warp audit on the same pass);
 //   * full refills leave through the bulk-copy engine from a rotated pool,
 //     16/64-byte aligned spans, exactly as in smem_impl.cuh.
-// Thread-to-column map: register slot k of lane l holds column
-// j = (k*G + l) mod N (l the lane in the WARP, not in the group), so in every
-// phase C store instruction the 32 lanes of the warp write 32 different banks
-// although the pools sit 4 or 8 KiB apart (with j = k*G + lane-in-group the
-// groups collided 4-way).  Only the last PPW slots can wrap.
+// Thread-to-column maps (k_group, "thread-to-column map"): chosen per dtype so
+// that the groups of a warp do not collide on shared-memory banks.  Measured
+// alternative (not kept): the 4 fp32 pools of a warp interleaved element by
+// element — conflict-free gathers and stores, but the pool is then no bulk-
+// copy source and per-value warp stores of 32-byte segments cost 4.8 LSU
+// cycles each: 1.49 ms per 2^30 against 1.04 ms with bulk copies.
 // Fills only (unit output of the pool's dtype, no restarts); every other
 // operation on such a handle runs on k_smem over the same device state.
 #include <type_traits>
@@ -52,7 +53,10 @@ template <typename T, int LOGN>
 struct Shape {
     static constexpr uint32_t N = 1u << LOGN;
     static constexpr uint32_t ES = (uint32_t)sizeof(T);
-    static constexpr uint32_t J = ES == 4 ? 32 : 16;  // columns per lane: 128 data registers
+#ifndef WG_GRP_J256  // fp32 4x256: columns per lane (32: 4 pools per warp; 16: 2 pools, 16 warps/SM)
+#define WG_GRP_J256 16
+#endif
+    static constexpr uint32_t J = ES == 4 ? (LOGN == 8 ? WG_GRP_J256 : 32) : 16;  // columns per lane
     static constexpr uint32_t G = N / J;              // lanes per pool
     static constexpr uint32_t PPW = 32 / G;           // pools per warp
     static_assert(G >= 8 && G <= 16, "group engine shapes: 2 or 4 pools per warp");
@@ -63,10 +67,14 @@ struct Shape {
     static constexpr uint32_t NVALS = 4 * N;
     static constexpr uint32_t CAP = NVALS - 1;
     static constexpr uint32_t VEC = 16 / ES;
-    // fp32 pools are interleaved element by element (PoolView below)
-    static constexpr bool IL = ES == 4;
-    // shared layout: word buffers | (pad to an aligned address) | pools
-    static constexpr uint32_t BYTES = PPW * kWBytes + (IL ? PPW : 1) * ABYTES + PPW * PBYTES;
+#ifndef WG_GRP_MINB64  // CTAs per SM the registers must allow at 64 data registers
+#define WG_GRP_MINB64 16
+#endif
+    static constexpr uint32_t MINB = (J * ES <= 64) ? WG_GRP_MINB64 : 8;
+    // fp32: residue-class thread-to-column map (k_group, "thread-to-column map")
+    static constexpr bool R4 = ES == 4;
+    // shared layout: word buffers | (pad to an ABYTES-aligned address) | pools
+    static constexpr uint32_t BYTES = PPW * kWBytes + ABYTES + PPW * PBYTES;
 };
 
 template <int B, int E, typename F>
@@ -205,42 +213,17 @@ __device__ __forceinline__ void transform(Cols<T, J>& u, uint32_t variant) {
 // Phase C bookkeeping of a bulk-emitting pass (smem_impl.cuh's PhaseC with
 // the group for the CTA).
 struct PhaseC {
-    uint32_t my_s;
     uint32_t j0, jend, jend_last;
     uint32_t src0;
 };
 
-// A group's pool in shared memory, natural flat index i = m*N + j:
-//   IL (fp32): the PPW pools of the warp interleaved element by element —
-//     pool q's value i at word i*PPW + q — so the bank of an access is
-//     (PPW*i + q) mod 32: the G lanes of a group (consecutive or odd-stride
-//     j) hit G distinct banks congruent to q mod PPW, and no two groups of
-//     the warp ever share a bank: gathers and stores are conflict-free by
-//     construction (separate pools: 3.1 wavefronts per gather, ncu);
-//   else (fp64: a group is a half-warp, which 64-bit accesses serve
-//     separately): contiguous, each array rotated by rot (bulk emission).
-template <typename T, bool IL, uint32_t PPW, uint32_t MASK>
-struct PoolView {
-    const T* p;  // IL: warp's pool block + q; else the group's pool
-    uint32_t rot;
-    __device__ __forceinline__ T operator[](uint32_t i) const {
-        if constexpr (IL)
-            return p[i * PPW];
-        else
-            return p[(i & ~MASK) | ((i + rot) & MASK)];
-    }
-};
-
 template <typename T, int LOGN>
-__global__ void __launch_bounds__(32, 8) k_group(const KernelArgs a) {
+__global__ void __launch_bounds__(32, Shape<T, LOGN>::MINB) k_group(const KernelArgs a) {
     using S = Shape<T, LOGN>;
     constexpr uint32_t N = S::N, G = S::G, J = S::J, ES = S::ES, VEC = S::VEC, PPW = S::PPW;
-    constexpr bool IL = S::IL;
+    constexpr bool R4 = S::R4;
+    constexpr uint32_t NT = J / PPW;  // R4: slots k = t*PPW + r, t < NT
     constexpr uint64_t CAP = S::CAP;
-    // element stride and array stride of a pool in shared memory (bytes)
-    constexpr uint32_t EST = IL ? PPW * ES : ES;
-    constexpr uint32_t AST = N * EST;
-    constexpr uint32_t MASKE = (N - 1) * EST;
     const uint32_t lane = threadIdx.x;
     const uint32_t q = lane / G, gl = lane % G;
     const uint32_t gmask = ((1u << G) - 1u) << (q * G);
@@ -253,34 +236,27 @@ __global__ void __launch_bounds__(32, 8) k_group(const KernelArgs a) {
 
     const uint32_t base_s = (uint32_t)__cvta_generic_to_shared(g_gsm);
     uint64_t* wbuf = reinterpret_cast<uint64_t*>(g_gsm + q * kWBytes);
-    // pools start on an AST-aligned shared address: a gather address is
+    // pools start on an ABYTES-aligned shared address: a gather address is
     // (index & mask) | base plus an immediate array offset
-    const uint32_t pool0_s = (base_s + PPW * kWBytes + AST - 1) / AST * AST;
-    const uint32_t pool_s = IL ? pool0_s + q * ES : pool0_s + q * S::PBYTES;
+    const uint32_t pool0_s =
+        (base_s + PPW * kWBytes + S::ABYTES - 1) / S::ABYTES * S::ABYTES;
+    const uint32_t pool_s = pool0_s + q * S::PBYTES;
     T* const pool = reinterpret_cast<T*>(g_gsm + (pool_s - base_s));
     uint64_t* tab = lg->table;
-    // this lane's slot-0 column: IL: j = k*G + gl; else j = (k*G + lane) mod N,
-    // so the 32 lanes of a store hit 32 banks although the pools sit 8 KiB apart
-    const uint32_t jl = IL ? gl : lane;
 
     // ---- load state -------------------------------------------------------
-    uint64_t pc = meta->pass_count, avail = meta->avail, emitted = meta->emitted;
+    // (loop state is kept in 32-bit counters: the host sends a fill here only
+    // when every pool's passes in the call stay below 2^31)
+    uint32_t avail = (uint32_t)meta->avail;  // <= CAP
     uint32_t act = meta->active;
     double tracked = meta->tracked[act], withheld = meta->withheld[act];
-    double prev_tracked = 0.0, prev_withheld = 0.0;
-    bool have_prev = false;
-    uint32_t r = lg->r;         // cursor at the start of the current word batch
-    uint64_t draws = lg->draws;
+    uint32_t r = lg->r;  // cursor at the start of the current word batch
     {
-        const T* srcp = static_cast<const T*>(a.buf[act]) + (uint64_t)p * S::NVALS;
-        if constexpr (IL) {
-            for (uint32_t i = gl; i < S::NVALS; i += G) pool[i * PPW] = srcp[i];
-        } else {
-            const uint4* src = reinterpret_cast<const uint4*>(srcp);
-            uint4* dst = reinterpret_cast<uint4*>(pool);
-            constexpr uint32_t NVEC = S::NVALS * ES / 16;
-            for (uint32_t i = gl; i < NVEC; i += G) dst[i] = src[i];
-        }
+        const uint4* src = reinterpret_cast<const uint4*>(static_cast<const T*>(a.buf[act]) +
+                                                          (uint64_t)p * S::NVALS);
+        uint4* dst = reinterpret_cast<uint4*>(pool);
+        constexpr uint32_t NVEC = S::NVALS * ES / 16;
+        for (uint32_t i = gl; i < NVEC; i += G) dst[i] = src[i];
     }
     __syncwarp(gmask);
 
@@ -289,47 +265,87 @@ __global__ void __launch_bounds__(32, 8) k_group(const KernelArgs a) {
         (uint64_t)p * a.lay.off_stride + (p < a.lay.off_extra ? p : a.lay.off_extra);
     T* const outv = static_cast<T*>(a.out) + out_base;
     const uint32_t f = a.f, mode = a.mode;
-    // bulk span alignment in elements: the ragged head (< bvec) stays inside
-    // column group 0, the tail (<= bvec + VEC - 2) inside the last one
+    // bulk span alignment in elements.  The ragged head (< bvec values) and
+    // tail (<= bvec + VEC - 2) leave through warp stores; they must lie in the
+    // slots that check for them: R4: t = 0 / t = NT-1 (32 columns each);
+    // else column group 0 / the last one (G columns)
     uint32_t bvec = VEC;
-    if constexpr (!IL) {
+    {
         const uint32_t want = a.bulk_emit / ES;
-        while (bvec * 2 <= want && bvec * 2 <= G && bvec * 2 + VEC <= G + 2) bvec *= 2;
+        if constexpr (R4) {
+            while (bvec * 2 <= want && bvec * 2 <= 16) bvec *= 2;
+        } else {
+            while (bvec * 2 <= want && bvec * 2 <= G && bvec * 2 + VEC <= G + 2) bvec *= 2;
+        }
     }
-    PeriodCounter drift;
-    drift.init(a.drift, pc);
+    // passes until the next drift audit (wallace.cpp:182-184: the refill that
+    // moves pass_count across a multiple of the period); ~0u: none in this call
+    uint32_t dper = 0, dleft = ~0u;
+    if (a.drift) {
+        const uint64_t until = a.drift - meta->pass_count % a.drift;
+        if (a.drift <= 0x7fffffffull) dper = (uint32_t)a.drift;
+        if (until <= 0x7fffffffull) dleft = (uint32_t)until;
+    }
 
-    uint64_t done = 0;
+    uint32_t take = 0;
     if (avail > 0 && len > 0) {
         // leftover of the live pool: flat [pos, pos + take)
-        const uint64_t take = umin64(len, avail);
-        const uint32_t pos = (uint32_t)(CAP - avail);
-        const PoolView<T, IL, PPW, S::MASK> v{pool, 0u};
-        for (uint32_t i = gl; i < (uint32_t)take; i += G) outv[i] = v[pos + i] + (T)0;
-        done = take;
+        take = (uint32_t)umin64(len, avail);
+        const uint32_t pos = (uint32_t)CAP - avail;
+        for (uint32_t i = gl; i < take; i += G) outv[i] = pool[pos + i] + (T)0;
         avail -= take;
     }
-    const uint64_t total_passes = (len - done + CAP - 1) / CAP * f;
-    uint64_t pass_i = 0;
-    uint32_t rot = 0;    // !IL: value j of each array sits at (j + rot) mod N
-    uint32_t wleft = 0;  // passes whose words are still in wbuf
-    uint32_t wpos = 0;   // next word in wbuf
-    uint32_t wcnt = 0;   // words of the current batch
+    // refills of this call: all full but the last, which exposes last_n values
+    const uint32_t nref = (uint32_t)((len - take + CAP - 1) / CAP);
+    const uint32_t last_n = nref ? (uint32_t)(len - take - (uint64_t)(nref - 1) * CAP) : 0u;
+    uint32_t ref_left = nref;
+    uint32_t passes_left = nref * a.f;
+    T* out_p = outv + take;
+
+    // ---- thread-to-column map ------------------------------------------------
+    // R4 (fp32): slot (t, r) of lane gl holds column j = 32 t + PPW gl + rr[r],
+    //   rr[r] = (r + cq) mod PPW.  The G lanes of a group then touch, in one
+    //   instruction, columns PPW apart: gathers (odd stride a) and stores hit G
+    //   distinct banks of ONE residue class mod PPW, so two groups collide
+    //   only when their classes coincide (whole-or-nothing: 2.1 wavefronts per
+    //   gather on average against 3.1 for consecutive columns) and never on
+    //   stores: cq = q - (output phase of the group's first refill), which
+    //   keeps (rr[r] + rot) mod PPW distinct across the groups for as long as
+    //   they refill in step.
+    // else (fp64: a group is a half-warp, which 64-bit accesses serve
+    //   separately): slot k holds column (k G + lane) mod N — lane of the
+    //   WARP, so the stores of a warp spread over all banks; the last PPW
+    //   slots can wrap.
+    uint32_t rr[PPW], jr[PPW];
+    if constexpr (R4) {
+        const uint32_t d0 = (uint32_t)(reinterpret_cast<uintptr_t>(out_p) / ES);
+        const uint32_t cq = q - d0;
+#pragma unroll
+        for (uint32_t x = 0; x < PPW; ++x) {
+            rr[x] = (x + cq) & (PPW - 1);
+            jr[x] = PPW * gl + rr[x];
+        }
+    }
+
+    uint32_t nstart = 0;  // passes whose words were consumed
+    uint32_t rot = 0;     // value j of each array sits at (j + rot) mod N
+    uint32_t wleft = 0;   // passes whose words are still in wbuf
+    uint32_t wpos = 0;    // next word in wbuf
+    uint32_t wcnt = 0;    // words of the current batch
     int err = 0;
+    bool scale_err = false;
     bool bulk_pending = false;
 
-    while (!err && done < len) {
+    while (ref_left > 0) {
         // refill (wallace.cpp:188-196), the exposed window fused into its last pass
-        const bool will_drift = drift.will_cross(f);
-        const uint32_t emit_n = (uint32_t)umin64(len - done, CAP);
-        T* const out_p = outv + done;
+        const bool will_drift = f >= dleft;
+        const uint32_t emit_n = ref_left == 1 ? last_n : (uint32_t)CAP;
         for (uint32_t i = 0; i < f; ++i) {
             if (wleft == 0) {
                 // next batch of uniform words, straight from the global lag table
-                const uint64_t left = total_passes - pass_i;
                 r += wcnt;
                 r = r >= kTable ? r - kTable : r;
-                wleft = left < kWPass ? (uint32_t)left : kWPass;
+                wleft = passes_left < kWPass ? passes_left : kWPass;
                 wcnt = wleft * 9;
                 wpos = 0;
 #pragma unroll 4
@@ -344,31 +360,30 @@ __global__ void __launch_bounds__(32, 8) k_group(const KernelArgs a) {
                 }
                 __syncwarp(gmask);
             }
-            ++pass_i;
-            const bool last_launch = pass_i == total_passes;
+            --passes_left;
+            const bool last_launch = passes_left == 0;
             const uint32_t en = i + 1 == f ? emit_n : 0u;
 
             // ---- this pass's parameters (docs/n4_spec.md §2) --------------
-            uint32_t ixb[4], stepb[4];
+            uint32_t strd[4], offs[4];
             uint32_t variant;
             {
                 const uint64_t* w = wbuf + wpos;
 #pragma unroll
                 for (int m = 0; m < 4; ++m) {
                     const uint32_t lo = m == 0 ? 3u : m == 1 ? 7u : m == 2 ? 13u : 19u;
-                    const uint32_t st = (w[m] >> 63) ? lo + (m == 0 ? 2u : 4u) : lo;
-                    const uint32_t off = (uint32_t)(w[4 + m] >> (64 - LOGN));
-                    ixb[m] = (st * jl + off + rot) * EST;
-                    stepb[m] = st * G * EST;
+                    strd[m] = (w[m] >> 63) ? lo + (m == 0 ? 2u : 4u) : lo;
+                    offs[m] = (uint32_t)(w[4 + m] >> (64 - LOGN));
                 }
                 variant = (uint32_t)(w[8] >> 63);
             }
             wpos += 9;
             --wleft;
-            draws += 9;
+            ++nstart;
             double scale = 0.0, target = 0.0;
             if (pass_scale(tracked, withheld, S::NVALS, mode, scale, target)) {
                 err = WRNG_GPU_ECORRUPT;  // wallace.cpp:59-61, after the draws
+                scale_err = true;
                 break;
             }
             // regenerate folds the scale into the matrix (wallace.cpp:116-117)
@@ -376,61 +391,92 @@ __global__ void __launch_bounds__(32, 8) k_group(const KernelArgs a) {
             if (last_launch) {
                 // the pre-pass pool becomes the inactive buffer (wallace.cpp:170-174)
                 T* prev = static_cast<T*>(a.buf[act]) + (uint64_t)p * S::NVALS;
-                const PoolView<T, IL, PPW, S::MASK> v{pool, rot};
+                const RotView<T> v{pool, S::MASK, rot};
                 for (uint32_t k = gl; k < S::NVALS; k += G) prev[k] = v[k];
-                prev_tracked = tracked;
-                prev_withheld = withheld;
-                have_prev = true;
+                if (gl == 0) {
+                    meta->tracked[act] = tracked;
+                    meta->withheld[act] = withheld;
+                }
             }
             // emission mode: 0 none, 2 warp stores of the window [0, en),
-            // 3 (contiguous pools) full refill through the bulk-copy engine
-            // (1: interleaved pools, full refill through warp stores)
-            const uint32_t md = en == 0 ? 0u : en == (uint32_t)CAP ? (IL ? 1u : 3u) : 2u;
+            // 3 full refill through the bulk-copy engine
+            const uint32_t md = en == 0 ? 0u : en == (uint32_t)CAP ? 3u : 2u;
             // new rotation: on a bulk-emitting pass, the output's 16-byte phase
             const uint32_t ophase = (uint32_t)(reinterpret_cast<uintptr_t>(out_p) / ES);
             const uint32_t rot2 = md == 3 ? ophase & (VEC - 1) : rot;
             PhaseC c;
-            c.my_s = pool_s + (jl + rot2) * EST;
-            // !IL: the last PPW slots can wrap: their columns and shared addresses
-            uint32_t wj[PPW], wa[PPW];
-            if constexpr (!IL) {
-#pragma unroll
-                for (uint32_t i2 = 0; i2 < PPW; ++i2) {
-                    wj[i2] = ((J - PPW + i2) * G + lane) & S::MASK;
-                    wa[i2] = (((wj[i2] + rot2) * ES) & S::MASKB) | pool_s;
-                }
+            {
                 const uint32_t ph = ophase & (bvec - 1);
                 c.j0 = (bvec - ph) & (bvec - 1);
                 c.jend = c.j0 + ((N - rot2 - c.j0) & ~(bvec - 1));
                 c.jend_last = c.j0 + ((umin32(N - rot2, N - 1) - c.j0) & ~(bvec - 1));
                 c.src0 = pool_s + (c.j0 + rot2) * ES;
             }
+            // store addresses: sb[x] + immediate for the slots that cannot
+            // wrap, wa[x] (masked) for those that can; wj[x]: their columns
+            uint32_t sb[R4 ? PPW : 1], wj[PPW], wa[PPW];
+            if constexpr (R4) {
+#pragma unroll
+                for (uint32_t x = 0; x < PPW; ++x) {
+                    sb[x] = pool_s + (jr[x] + rot2) * ES;
+                    wj[x] = (NT - 1) * 32 + jr[x];
+                    wa[x] = (((wj[x] + rot2) * ES) & S::MASKB) | pool_s;
+                }
+            } else {
+                sb[0] = pool_s + (lane + rot2) * ES;
+#pragma unroll
+                for (uint32_t x = 0; x < PPW; ++x) {
+                    wj[x] = ((J - PPW + x) * G + lane) & S::MASK;
+                    wa[x] = (((wj[x] + rot2) * ES) & S::MASKB) | pool_s;
+                }
+            }
 
             // ---- phase B: gather every column, then the transform ---------
             Cols<T, J> u;
-            if constexpr (ES == 4) {
-                sfor<0, (int)J / 2>([&](auto kc) {
-                    constexpr int kp = decltype(kc)::value;
-                    float g[4][2];
-                    sfor<0, 2>([&](auto hc) {
-                        constexpr int h = decltype(hc)::value;
+            if constexpr (R4) {
+                // pairs of residues outside, t inside: 2 x 4 running indices
+                sfor<0, (int)PPW / 2>([&](auto rpc) {
+                    constexpr int rp = decltype(rpc)::value;
+                    uint32_t ix[2][4], stp[4];
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        const uint32_t bs = strd[m] * PPW * gl + offs[m] + rot;
+                        ix[0][m] = (bs + strd[m] * rr[2 * rp]) * ES;
+                        ix[1][m] = (bs + strd[m] * rr[2 * rp + 1]) * ES;
+                        stp[m] = strd[m] * 32 * ES;
+                    }
+                    sfor<0, (int)NT>([&](auto tc) {
+                        constexpr int t = decltype(tc)::value;
+                        constexpr int kp = (t * (int)PPW + 2 * rp) / 2;
+                        float g[4][2];
+                        sfor<0, 2>([&](auto hc) {
+                            constexpr int h = decltype(hc)::value;
+                            sfor<0, 4>([&](auto mc) {
+                                constexpr int m = decltype(mc)::value;
+                                g[m][h] = lds<float, (uint32_t)m * S::ABYTES>(
+                                    (ix[h][m] & S::MASKB) | pool_s);
+                                ix[h][m] += stp[m];
+                            });
+                        });
                         sfor<0, 4>([&](auto mc) {
                             constexpr int m = decltype(mc)::value;
-                            g[m][h] = lds<float, (uint32_t)m * AST>((ixb[m] & MASKE) | pool_s);
-                            ixb[m] += stepb[m];
+                            u.v[m][kp] = f2_pack(g[m][0], g[m][1]);
                         });
-                    });
-                    sfor<0, 4>([&](auto mc) {
-                        constexpr int m = decltype(mc)::value;
-                        u.v[m][kp] = f2_pack(g[m][0], g[m][1]);
                     });
                 });
             } else {
+                uint32_t ixb[4], stepb[4];
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    ixb[m] = (strd[m] * lane + offs[m] + rot) * ES;  // slot 0: column lane
+                    stepb[m] = strd[m] * G * ES;
+                }
                 sfor<0, (int)J>([&](auto kc) {
                     constexpr int k = decltype(kc)::value;
                     sfor<0, 4>([&](auto mc) {
                         constexpr int m = decltype(mc)::value;
-                        u.v[m][k] = lds<T, (uint32_t)m * AST>((ixb[m] & MASKE) | pool_s);
+                        u.v[m][k] =
+                            lds<T, (uint32_t)m * S::ABYTES>((ixb[m] & S::MASKB) | pool_s);
                         ixb[m] += stepb[m];
                     });
                 });
@@ -441,12 +487,13 @@ __global__ void __launch_bounds__(32, 8) k_group(const KernelArgs a) {
             if (bulk_pending && gl == 0) bulk_wait_read();
             __syncwarp(gmask);
 
-            // ---- phase C: scale, store in place, emit ---------------------
+            // ---- phase C: scale, store in place (rotated), emit -----------
             double wh = 0.0;
-            T* const ob = out_p + jl;
             // one instantiation per emission mode MD
             auto phase_c = [&](auto mdc) {
                 constexpr uint32_t MD = decltype(mdc)::value;
+                // value y of array m in slot k: into the pool, and to the output
+                // where this lane emits it itself
                 auto put = [&](auto mc, auto kc, T y) {
                     constexpr int m = decltype(mc)::value;
                     constexpr int k = decltype(kc)::value;
@@ -454,26 +501,25 @@ __global__ void __launch_bounds__(32, 8) k_group(const KernelArgs a) {
                     // holds it, being the bulk source
                     const T e = MD == 0 ? y : y + (T)0;
                     const T sv = MD == 3 ? e : y;
-                    if constexpr (IL || k < (int)(J - PPW)) {
-                        constexpr uint32_t col = (uint32_t)m * N + (uint32_t)k * G;
-                        sts<T, (uint32_t)m * AST + (uint32_t)k * G * EST>(c.my_s, sv);
-                        if constexpr (MD == 3 && k == 0) {  // ragged head (group 0's lanes)
-                            if (lane < c.j0) ob[col] = e;
+                    constexpr int x = R4 ? k % (int)PPW : k - (int)(J - PPW);
+                    constexpr bool first = R4 ? k < (int)PPW : k == 0;
+                    constexpr bool last = R4 ? k >= (int)(J - PPW) : k >= (int)(J - PPW);
+                    if constexpr (!last) {
+                        constexpr uint32_t o = R4 ? (uint32_t)(k / (int)PPW) * 32 : (uint32_t)k * G;
+                        const uint32_t j = o + (R4 ? jr[x] : lane);  // no wrap
+                        sts<T, (uint32_t)m * S::ABYTES + o * ES>(sb[R4 ? x : 0], sv);
+                        if constexpr (MD == 3 && first) {  // ragged head
+                            if (j < c.j0) out_p[(uint32_t)m * N + j] = e;
                         }
                         if constexpr (MD == 2) {
-                            if (col + jl < en) ob[col] = e;
+                            if ((uint32_t)m * N + j < en) out_p[(uint32_t)m * N + j] = e;
                         }
-                        if constexpr (MD == 1) {  // everything but the withheld value
-                            if (!(m == 3 && k == (int)J - 1) || jl != G - 1) ob[col] = e;
-                        }
-                        if constexpr (IL && m == 3 && k == (int)J - 1) wh = (double)y;
                     } else {
-                        constexpr int i2 = k - (int)(J - PPW);
-                        const uint32_t j = wj[i2];
-                        sts<T, (uint32_t)m * AST>(wa[i2], sv);
-                        if constexpr (MD == 3) {  // ragged head (column 0), tail (last column)
+                        const uint32_t j = wj[x];
+                        sts<T, (uint32_t)m * S::ABYTES>(wa[x], sv);
+                        if constexpr (MD == 3) {  // ragged tail (and head, !R4)
                             const bool own =
-                                j < c.j0 ||
+                                (!R4 && j < c.j0) ||
                                 (m == 3 ? (j >= c.jend_last && j != N - 1) : j >= c.jend);
                             if (own) out_p[(uint32_t)m * N + j] = e;
                         }
@@ -486,15 +532,26 @@ __global__ void __launch_bounds__(32, 8) k_group(const KernelArgs a) {
                     }
                 };
                 if constexpr (ES == 4) {
-                    const f2_t C = f2_pack(c0, c0);
+                    const f2_t C = f2_pack(c0, c0), Z = f2_pack(0.0f, 0.0f);
                     sfor<0, (int)J / 2>([&](auto kc) {
                         constexpr int kp = decltype(kc)::value;
+                        constexpr int k0 = 2 * kp;
                         sfor<0, 4>([&](auto mc) {
                             constexpr int m = decltype(mc)::value;
+                            const f2_t Y = f2_mul(C, u.v[m][kp]);
                             float y0, y1;
-                            f2_unpack(f2_mul(C, u.v[m][kp]), y0, y1);
-                            put(mc, std::integral_constant<int, 2 * kp>{}, y0);
-                            put(mc, std::integral_constant<int, 2 * kp + 1>{}, y1);
+                            if constexpr (MD == 3 && k0 >= (int)PPW && k0 + 1 < (int)(J - PPW)) {
+                                // nothing to emit here: only the pool's emitted form
+                                f2_unpack(f2_add(Y, Z), y0, y1);
+                                constexpr uint32_t o = (uint32_t)m * S::ABYTES +
+                                                       (uint32_t)(k0 / (int)PPW) * 32 * ES;
+                                sts<T, o>(sb[k0 % (int)PPW], y0);
+                                sts<T, o>(sb[(k0 + 1) % (int)PPW], y1);
+                            } else {
+                                f2_unpack(Y, y0, y1);
+                                put(mc, std::integral_constant<int, k0>{}, y0);
+                                put(mc, std::integral_constant<int, k0 + 1>{}, y1);
+                            }
                         });
                     });
                 } else {
@@ -509,10 +566,8 @@ __global__ void __launch_bounds__(32, 8) k_group(const KernelArgs a) {
             };
             if (md == 0)
                 phase_c(std::integral_constant<uint32_t, 0>{});
-            else if (!IL && md == 3)
+            else if (md == 3)
                 phase_c(std::integral_constant<uint32_t, 3>{});
-            else if (IL && md == 1)
-                phase_c(std::integral_constant<uint32_t, 1>{});
             else
                 phase_c(std::integral_constant<uint32_t, 2>{});
             if (md == 3) fence_async_smem();  // generic -> async proxy
@@ -520,7 +575,6 @@ __global__ void __launch_bounds__(32, 8) k_group(const KernelArgs a) {
             withheld = __shfl_sync(gmask, wh, G - 1, G);       // wallace.cpp:136
             act ^= 1u;
             rot = rot2;
-            ++pc;
             __syncwarp(gmask);
             if (md == 3) {
                 if (gl == 0) {
@@ -539,17 +593,32 @@ __global__ void __launch_bounds__(32, 8) k_group(const KernelArgs a) {
             }
         }
         if (err) break;
-        drift.advance(f);
-        avail = CAP;
+        if (will_drift) {
+            const uint32_t over = f - dleft;
+            dleft = dper ? dper - over % dper : ~0u;
+        } else if (dleft != ~0u) {
+            dleft -= f;
+        }
+        avail = (uint32_t)CAP;
         if (will_drift) {
             // wallace.cpp:225-234 with Pool::direct_sumsq order (wallace.cpp:13-18)
             double rec = 0.0;
             if (gl == 0) {
-                const PoolView<T, IL, PPW, S::MASK> v{pool, rot};
+                // natural order of a rotated array: positions [rot, N), then [0, rot)
+                // (rot < VEC): straight runs, no per-element index arithmetic
+#pragma unroll 1
+                for (uint32_t m = 0; m < 4; ++m) {
+                    const T* am = pool + m * N;
+                    const uint32_t head = N - VEC;  // a multiple of 8
 #pragma unroll 8
-                for (uint32_t k = 0; k < S::NVALS; ++k) {
-                    const double d = (double)v[k];
-                    rec = rec + d * d;
+                    for (uint32_t k = 0; k < head; ++k) {
+                        const double d = (double)am[rot + k];
+                        rec = rec + d * d;
+                    }
+                    for (uint32_t k = head; k < N; ++k) {
+                        const double d = (double)am[(rot + k) & S::MASK];
+                        rec = rec + d * d;
+                    }
                 }
             }
             rec = __shfl_sync(gmask, rec, 0, G);
@@ -560,10 +629,10 @@ __global__ void __launch_bounds__(32, 8) k_group(const KernelArgs a) {
             }
             tracked = rec;
         }
-        done += emit_n;
+        out_p += emit_n;
         avail -= emit_n;
+        --ref_left;
     }
-    if (!err) emitted += len;
 
     // ---- write back -------------------------------------------------------
     if (bulk_pending && gl == 0) bulk_wait_all();  // bulk copies complete before exit
@@ -579,33 +648,29 @@ __global__ void __launch_bounds__(32, 8) k_group(const KernelArgs a) {
     r += wpos;
     r = r >= kTable ? r - kTable : r;
     __syncwarp(gmask);
-    if (pass_i > 0) {
+    if (nstart > 0) {
         T* dst = static_cast<T*>(a.buf[act]) + (uint64_t)p * S::NVALS;
-        if (!IL && rot == 0) {
+        if (rot == 0) {
             constexpr uint32_t NVEC = S::NVALS * ES / 16;
             for (uint32_t i = gl; i < NVEC; i += G)
                 reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(pool)[i];
         } else {  // back to natural order
-            const PoolView<T, IL, PPW, S::MASK> v{pool, rot};
+            const RotView<T> v{pool, S::MASK, rot};
             for (uint32_t i = gl; i < S::NVALS; i += G) dst[i] = v[i];
         }
     }
     if (gl == 0) {
         lg->r = r;
-        lg->draws = draws;
+        lg->draws += (uint64_t)nstart * 9;
         meta->tracked[act] = tracked;
         meta->withheld[act] = withheld;
-        if (have_prev) {
-            meta->tracked[act ^ 1u] = prev_tracked;
-            meta->withheld[act ^ 1u] = prev_withheld;
-        }
         meta->active = act;
-        meta->pass_count = pc;
+        meta->pass_count += nstart - (scale_err ? 1u : 0u);
         meta->avail = avail;
-        meta->emitted = emitted;
+        if (!err) meta->emitted += len;
         meta->error = (uint32_t)err;
         meta->restart_pending = 0u;
-        meta->fill_done = done;
+        meta->fill_done = err ? take + (uint64_t)(nref - ref_left) * CAP : len;
     }
 }
 
