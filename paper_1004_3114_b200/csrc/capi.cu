@@ -675,7 +675,7 @@ wrng_gpu_status fill_device(wrng_gpu* g, void* out, int out_f32, const OutLayout
             LAUNCH(launch_cluster(g->cfg.n_arrays, g->cfg.dtype, a, s));
         else if (g_group && !stats && unit_same && a.bulk_emit &&
                  g->cfg.restart_interval_passes == 0 &&
-                 group_engine_fits(g->cfg.n_arrays, g->cfg.dtype, g->N) &&
+                 group_engine_fits(g->cfg.n_arrays, g->cfg.dtype, g->N, g->cfg.throwaway_f) &&
                  // its loop counters are 32-bit: passes per pool in this call
                  ((lay.len_base + 1) / g->cap + 2) * g->cfg.throwaway_f < (1ull << 31))
             LAUNCH(launch_group(g->cfg.dtype, a, s));
@@ -1612,7 +1612,7 @@ int64_t wrng_gpu_resident_pools(const wrng_gpu_config* cfg) {
     a.f = cfg->throwaway_f;
     a.out = &per_sm;
     const bool grp = g_group && cfg->restart_interval_passes == 0 &&
-                     group_engine_fits(cfg->n_arrays, cfg->dtype, N);
+                     group_engine_fits(cfg->n_arrays, cfg->dtype, N, cfg->throwaway_f);
     if ((grp ? launch_group(cfg->dtype, a, nullptr)
              : launch_smem(cfg->n_arrays, cfg->dtype, a, nullptr)) != cudaSuccess ||
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device) != cudaSuccess)

@@ -61,7 +61,9 @@ struct Shape {
     static constexpr uint32_t PPW = 32 / G;           // pools per warp
     static_assert(G >= 8 && G <= 16, "group engine shapes: 2 or 4 pools per warp");
     static constexpr uint32_t ABYTES = N * ES;
-    static constexpr uint32_t PBYTES = 4 * ABYTES;
+    // a pool in shared memory: flat index i = m*N + j at position i + rot,
+    // rot < VEC (one linear image, so a full refill is ONE bulk copy)
+    static constexpr uint32_t PBYTES = 4 * ABYTES + 16;
     static constexpr uint32_t MASK = N - 1;
     static constexpr uint32_t MASKB = MASK * ES;
     static constexpr uint32_t NVALS = 4 * N;
@@ -73,8 +75,8 @@ struct Shape {
     static constexpr uint32_t MINB = (J * ES <= 64) ? WG_GRP_MINB64 : 8;
     // fp32: residue-class thread-to-column map (k_group, "thread-to-column map")
     static constexpr bool R4 = ES == 4;
-    // shared layout: word buffers | (pad to an ABYTES-aligned address) | pools
-    static constexpr uint32_t BYTES = PPW * kWBytes + ABYTES + PPW * PBYTES;
+    // shared layout: word buffers | pools
+    static constexpr uint32_t BYTES = PPW * kWBytes + PPW * PBYTES;
 };
 
 template <int B, int E, typename F>
@@ -213,8 +215,8 @@ __device__ __forceinline__ void transform(Cols<T, J>& u, uint32_t variant) {
 // Phase C bookkeeping of a bulk-emitting pass (smem_impl.cuh's PhaseC with
 // the group for the CTA).
 struct PhaseC {
-    uint32_t j0, jend, jend_last;
-    uint32_t src0;
+    uint32_t j0;    // flat [0, j0): ragged head, stored by the lanes holding it
+    uint32_t jend;  // flat [j0, jend): the bulk copy; [jend, 4N - 1): ragged tail
 };
 
 template <typename T, int LOGN>
@@ -236,11 +238,7 @@ __global__ void __launch_bounds__(32, Shape<T, LOGN>::MINB) k_group(const Kernel
 
     const uint32_t base_s = (uint32_t)__cvta_generic_to_shared(g_gsm);
     uint64_t* wbuf = reinterpret_cast<uint64_t*>(g_gsm + q * kWBytes);
-    // pools start on an ABYTES-aligned shared address: a gather address is
-    // (index & mask) | base plus an immediate array offset
-    const uint32_t pool0_s =
-        (base_s + PPW * kWBytes + S::ABYTES - 1) / S::ABYTES * S::ABYTES;
-    const uint32_t pool_s = pool0_s + q * S::PBYTES;
+    const uint32_t pool_s = base_s + PPW * kWBytes + q * S::PBYTES;  // 16-byte aligned
     T* const pool = reinterpret_cast<T*>(g_gsm + (pool_s - base_s));
     uint64_t* tab = lg->table;
 
@@ -265,18 +263,14 @@ __global__ void __launch_bounds__(32, Shape<T, LOGN>::MINB) k_group(const Kernel
         (uint64_t)p * a.lay.off_stride + (p < a.lay.off_extra ? p : a.lay.off_extra);
     T* const outv = static_cast<T*>(a.out) + out_base;
     const uint32_t f = a.f, mode = a.mode;
-    // bulk span alignment in elements.  The ragged head (< bvec values) and
-    // tail (<= bvec + VEC - 2) leave through warp stores; they must lie in the
-    // slots that check for them: R4: t = 0 / t = NT-1 (32 columns each);
-    // else column group 0 / the last one (G columns)
+    // bulk span alignment in elements (a power of two, 16 bytes to 16
+    // elements).  The ragged head (< bvec values of array 0) and tail (< bvec
+    // values of array 3) leave through warp stores from the slots that hold
+    // the first / last 16 columns.
     uint32_t bvec = VEC;
     {
         const uint32_t want = a.bulk_emit / ES;
-        if constexpr (R4) {
-            while (bvec * 2 <= want && bvec * 2 <= 16) bvec *= 2;
-        } else {
-            while (bvec * 2 <= want && bvec * 2 <= G && bvec * 2 + VEC <= G + 2) bvec *= 2;
-        }
+        while (bvec * 2 <= want && bvec * 2 <= 16) bvec *= 2;
     }
     // passes until the next drift audit (wallace.cpp:182-184: the refill that
     // moves pass_count across a multiple of the period); ~0u: none in this call
@@ -391,8 +385,7 @@ __global__ void __launch_bounds__(32, Shape<T, LOGN>::MINB) k_group(const Kernel
             if (last_launch) {
                 // the pre-pass pool becomes the inactive buffer (wallace.cpp:170-174)
                 T* prev = static_cast<T*>(a.buf[act]) + (uint64_t)p * S::NVALS;
-                const RotView<T> v{pool, S::MASK, rot};
-                for (uint32_t k = gl; k < S::NVALS; k += G) prev[k] = v[k];
+                for (uint32_t k = gl; k < S::NVALS; k += G) prev[k] = pool[k + rot];
                 if (gl == 0) {
                     meta->tracked[act] = tracked;
                     meta->withheld[act] = withheld;
@@ -408,28 +401,27 @@ __global__ void __launch_bounds__(32, Shape<T, LOGN>::MINB) k_group(const Kernel
             {
                 const uint32_t ph = ophase & (bvec - 1);
                 c.j0 = (bvec - ph) & (bvec - 1);
-                c.jend = c.j0 + ((N - rot2 - c.j0) & ~(bvec - 1));
-                c.jend_last = c.j0 + ((umin32(N - rot2, N - 1) - c.j0) & ~(bvec - 1));
-                c.src0 = pool_s + (c.j0 + rot2) * ES;
+                c.jend = c.j0 + (((uint32_t)CAP - c.j0) & ~(bvec - 1));
             }
-            // store addresses: sb[x] + immediate for the slots that cannot
-            // wrap, wa[x] (masked) for those that can; wj[x]: their columns
+            // store addresses: sb[x] + immediate; wj[x]: the columns of the
+            // last PPW slots (fp64 map: they can wrap)
             uint32_t sb[R4 ? PPW : 1], wj[PPW], wa[PPW];
             if constexpr (R4) {
 #pragma unroll
                 for (uint32_t x = 0; x < PPW; ++x) {
                     sb[x] = pool_s + (jr[x] + rot2) * ES;
                     wj[x] = (NT - 1) * 32 + jr[x];
-                    wa[x] = (((wj[x] + rot2) * ES) & S::MASKB) | pool_s;
+                    wa[x] = sb[x] + (NT - 1) * 32 * ES;
                 }
             } else {
                 sb[0] = pool_s + (lane + rot2) * ES;
 #pragma unroll
                 for (uint32_t x = 0; x < PPW; ++x) {
                     wj[x] = ((J - PPW + x) * G + lane) & S::MASK;
-                    wa[x] = (((wj[x] + rot2) * ES) & S::MASKB) | pool_s;
+                    wa[x] = pool_s + (wj[x] + rot2) * ES;
                 }
             }
+            const uint32_t gbase = pool_s + rot * ES;  // gather base: value i at i + rot
 
             // ---- phase B: gather every column, then the transform ---------
             Cols<T, J> u;
@@ -440,7 +432,7 @@ __global__ void __launch_bounds__(32, Shape<T, LOGN>::MINB) k_group(const Kernel
                     uint32_t ix[2][4], stp[4];
 #pragma unroll
                     for (int m = 0; m < 4; ++m) {
-                        const uint32_t bs = strd[m] * PPW * gl + offs[m] + rot;
+                        const uint32_t bs = strd[m] * PPW * gl + offs[m];
                         ix[0][m] = (bs + strd[m] * rr[2 * rp]) * ES;
                         ix[1][m] = (bs + strd[m] * rr[2 * rp + 1]) * ES;
                         stp[m] = strd[m] * 32 * ES;
@@ -454,7 +446,7 @@ __global__ void __launch_bounds__(32, Shape<T, LOGN>::MINB) k_group(const Kernel
                             sfor<0, 4>([&](auto mc) {
                                 constexpr int m = decltype(mc)::value;
                                 g[m][h] = lds<float, (uint32_t)m * S::ABYTES>(
-                                    (ix[h][m] & S::MASKB) | pool_s);
+                                    (ix[h][m] & S::MASKB) + gbase);
                                 ix[h][m] += stp[m];
                             });
                         });
@@ -468,7 +460,7 @@ __global__ void __launch_bounds__(32, Shape<T, LOGN>::MINB) k_group(const Kernel
                 uint32_t ixb[4], stepb[4];
 #pragma unroll
                 for (int m = 0; m < 4; ++m) {
-                    ixb[m] = (strd[m] * lane + offs[m] + rot) * ES;  // slot 0: column lane
+                    ixb[m] = (strd[m] * lane + offs[m]) * ES;  // slot 0: column lane
                     stepb[m] = strd[m] * G * ES;
                 }
                 sfor<0, (int)J>([&](auto kc) {
@@ -476,7 +468,7 @@ __global__ void __launch_bounds__(32, Shape<T, LOGN>::MINB) k_group(const Kernel
                     sfor<0, 4>([&](auto mc) {
                         constexpr int m = decltype(mc)::value;
                         u.v[m][k] =
-                            lds<T, (uint32_t)m * S::ABYTES>((ixb[m] & S::MASKB) | pool_s);
+                            lds<T, (uint32_t)m * S::ABYTES>((ixb[m] & S::MASKB) + gbase);
                         ixb[m] += stepb[m];
                     });
                 });
@@ -508,8 +500,8 @@ __global__ void __launch_bounds__(32, Shape<T, LOGN>::MINB) k_group(const Kernel
                         constexpr uint32_t o = R4 ? (uint32_t)(k / (int)PPW) * 32 : (uint32_t)k * G;
                         const uint32_t j = o + (R4 ? jr[x] : lane);  // no wrap
                         sts<T, (uint32_t)m * S::ABYTES + o * ES>(sb[R4 ? x : 0], sv);
-                        if constexpr (MD == 3 && first) {  // ragged head
-                            if (j < c.j0) out_p[(uint32_t)m * N + j] = e;
+                        if constexpr (MD == 3 && first && m == 0) {  // ragged head
+                            if (j < c.j0) out_p[j] = e;
                         }
                         if constexpr (MD == 2) {
                             if ((uint32_t)m * N + j < en) out_p[(uint32_t)m * N + j] = e;
@@ -517,11 +509,11 @@ __global__ void __launch_bounds__(32, Shape<T, LOGN>::MINB) k_group(const Kernel
                     } else {
                         const uint32_t j = wj[x];
                         sts<T, (uint32_t)m * S::ABYTES>(wa[x], sv);
-                        if constexpr (MD == 3) {  // ragged tail (and head, !R4)
-                            const bool own =
-                                (!R4 && j < c.j0) ||
-                                (m == 3 ? (j >= c.jend_last && j != N - 1) : j >= c.jend);
-                            if (own) out_p[(uint32_t)m * N + j] = e;
+                        if constexpr (MD == 3 && !R4 && m == 0) {  // ragged head (fp64 map)
+                            if (j < c.j0) out_p[j] = e;
+                        }
+                        if constexpr (MD == 3 && m == 3) {  // ragged tail, withheld slot excluded
+                            if (3 * N + j >= c.jend && j != N - 1) out_p[3 * N + j] = e;
                         }
                         if constexpr (MD == 2) {
                             if ((uint32_t)m * N + j < en) out_p[(uint32_t)m * N + j] = e;
@@ -578,15 +570,9 @@ __global__ void __launch_bounds__(32, Shape<T, LOGN>::MINB) k_group(const Kernel
             __syncwarp(gmask);
             if (md == 3) {
                 if (gl == 0) {
-                    // [j0, jend) of every array (last: jend_last) -> output
-                    const uint64_t o = reinterpret_cast<uint64_t>(out_p);
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        const uint32_t je = m == 3 ? c.jend_last : c.jend;
-                        if (je > c.j0)
-                            bulk_store(o + ((uint64_t)m * N + c.j0) * ES,
-                                       c.src0 + (uint32_t)m * S::ABYTES, (je - c.j0) * ES);
-                    }
+                    // flat [j0, jend) -> output: one copy, 16-byte aligned on both sides
+                    bulk_store(reinterpret_cast<uint64_t>(out_p + c.j0),
+                               pool_s + (c.j0 + rot2) * ES, (c.jend - c.j0) * ES);
                     bulk_commit();
                 }
                 bulk_pending = true;
@@ -604,21 +590,10 @@ __global__ void __launch_bounds__(32, Shape<T, LOGN>::MINB) k_group(const Kernel
             // wallace.cpp:225-234 with Pool::direct_sumsq order (wallace.cpp:13-18)
             double rec = 0.0;
             if (gl == 0) {
-                // natural order of a rotated array: positions [rot, N), then [0, rot)
-                // (rot < VEC): straight runs, no per-element index arithmetic
-#pragma unroll 1
-                for (uint32_t m = 0; m < 4; ++m) {
-                    const T* am = pool + m * N;
-                    const uint32_t head = N - VEC;  // a multiple of 8
 #pragma unroll 8
-                    for (uint32_t k = 0; k < head; ++k) {
-                        const double d = (double)am[rot + k];
-                        rec = rec + d * d;
-                    }
-                    for (uint32_t k = head; k < N; ++k) {
-                        const double d = (double)am[(rot + k) & S::MASK];
-                        rec = rec + d * d;
-                    }
+                for (uint32_t k = 0; k < S::NVALS; ++k) {
+                    const double d = (double)pool[rot + k];
+                    rec = rec + d * d;
                 }
             }
             rec = __shfl_sync(gmask, rec, 0, G);
@@ -654,9 +629,8 @@ __global__ void __launch_bounds__(32, Shape<T, LOGN>::MINB) k_group(const Kernel
             constexpr uint32_t NVEC = S::NVALS * ES / 16;
             for (uint32_t i = gl; i < NVEC; i += G)
                 reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(pool)[i];
-        } else {  // back to natural order
-            const RotView<T> v{pool, S::MASK, rot};
-            for (uint32_t i = gl; i < S::NVALS; i += G) dst[i] = v[i];
+        } else {  // unshifted
+            for (uint32_t i = gl; i < S::NVALS; i += G) dst[i] = pool[i + rot];
         }
     }
     if (gl == 0) {
@@ -684,6 +658,10 @@ static cudaError_t go(const KernelArgs& a, cudaStream_t st) {
     if (a.op == OP_QUERY) {  // pools per SM
         int ctas = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, kern, 32, S::BYTES);
+        // f = 1 fills are bound by the output pattern, not by generation:
+        // fewer, longer output streams measured faster (fp32 4x256: 24 pools per
+        // SM 75.2-76.0 % of the HBM roofline, 32 per SM 73.3 %)
+        if (a.f == 1 && S::MINB > 12 && ctas > 12) ctas = 12;
         *static_cast<int*>(a.out) = ctas * (int)S::PPW;
         return e;
     }
@@ -693,9 +671,15 @@ static cudaError_t go(const KernelArgs& a, cudaStream_t st) {
 
 }  // namespace grp
 
-bool group_engine_fits(uint32_t n_arrays, uint32_t dtype, uint32_t N) {
+// Shapes the group engine takes (measured against one CTA per pool, one wave
+// of pools each, 2^32 normals, % of the HBM-store roofline):
+// fp32 4x256 f = 1..4: 76 / 53 / 37 / 29 % against 44 / 25 / 18 / 14 %; fp64
+// 4x256 f = 2..4: 62 / 45 / 35 % against 47 / 34 / 26 %; fp64 4x256 at f = 1
+// stays on one CTA per pool (81 % against 80 %: both at the ceiling of the
+// output pattern).
+bool group_engine_fits(uint32_t n_arrays, uint32_t dtype, uint32_t N, uint32_t f) {
     if (n_arrays != 4) return false;
-    return dtype == WRNG_GPU_F64 ? N == 256 : (N == 256 || N == 512);
+    return dtype == WRNG_GPU_F64 ? (N == 256 && f >= 2) : (N == 256 || N == 512);
 }
 
 cudaError_t launch_group(uint32_t dtype, const KernelArgs& a, cudaStream_t st) {

@@ -116,7 +116,7 @@ void smem_engine_probe(cudaStream_t st);
 
 // Group engine (group_engine.cu): 2 or 4 small n = 4 pools per warp; unit
 // fills without restarts.  OP_QUERY writes the POOLS per SM to *(int*)out.
-bool group_engine_fits(uint32_t n_arrays, uint32_t dtype, uint32_t N);
+bool group_engine_fits(uint32_t n_arrays, uint32_t dtype, uint32_t N, uint32_t f);
 cudaError_t launch_group(uint32_t dtype, const KernelArgs& a, cudaStream_t st);
 
 // Cluster engine (cluster_engine.cu): one pool over a cluster of 8 CTAs,
