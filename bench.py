@@ -8,7 +8,8 @@ Workload at every N (one curve): the C4 shard ("c4w")
 generate N x 2^34; at N = 4 that is exactly C4's 2^36 split evenly), no
 inter-GPU communication on the generation path.  At N = 1 that is C3's
 shape with C4's seed; the N = 1 line also carries the exact C3 config (seed
-2024), C4 at N = 1 (2^36 per step, strong-scaling form), C1, C2 and the GPU
+2024), C4 at N = 1 (2^36 per step, strong-scaling form), C1, C2, C5's
+smallest pools (fp32 / fp64 4x256, R = 1, one resident wave) and the GPU
 at the reference's only mode (n = 2 fp64, "matched_reference"), all
 measured in the same run.  `--config c1 | c2 | c3 | c4` makes one of them
 the line's workload instead (c4: 2^36 split evenly, strong scaling).
@@ -534,6 +535,17 @@ def main():
         line["c2"] = sub_bench("c2", CONFIGS["c2"], 7, 1 << 30, 3, 1, local, dev,
                                e2e_n=1 << 27)
         line["c1"] = sub_bench("c1", CONFIGS["c1"], 12345, 1 << 24, 3, 1, local, dev)
+        # C5's smallest pools (configs[4], R = 1): the group engine, several
+        # pools per warp, one resident wave
+        from paper_1004_3114_b200 import WallaceConfig, resident_pools
+        for nm, dt in (("c5_f32_4x256", "f32"), ("c5_f64_4x256", "f64")):
+            c5 = dict(n_arrays=4, dtype=dt, pool_exponent=8, throwaway_f=1, seed=2024,
+                      total=1 << 32, pools=1)
+            c5["pools"] = resident_pools(WallaceConfig(
+                pool_exponent=8, throwaway_f=1, n_arrays=4, dtype=dt, device=local))
+            c5["desc"] = (f"C5 {dt} n=4 4x256 pools, R=1, chi rescale on, {c5['pools']} pools "
+                          f"(one resident wave), seed 2024, 2^32 normals per step")
+            line[nm] = sub_bench(nm, c5, 2024, 1 << 32, 3, 2, local, dev)
         line["matched_reference"] = sub_bench(
             "matched", MATCHED, 2024, MATCHED["total"], 3, 2, local, dev, e2e_n=1 << 28)
         line["matched_reference"]["note"] = (

@@ -3,6 +3,12 @@
 // no emission overlaps the non-emitting passes and twice the warps per SM
 // win (BASELINE configs[4] sweep).
 #define WG_DATA_REGS 64
+// 128 registers per thread -> 8 CTAs (16 warps) per SM for a 4x1024 fp32 pool:
+// f >= 2 fills are generation-bound, occupancy wins (C5 fp32 4x1024 R = 2:
+// 50.9 % at 8 CTAs per SM against 39.7 % at the 255-register budget's 4).
+// Larger pools gain nothing from this engine (shared memory, not registers,
+// limits their CTAs per SM: fp32 4x4096 R = 2 42.7 % here against 45.3 %).
+#define WG_RBUDGET_MIN 128
 #define WG_SMEM_NS r64
 #include "smem_impl.cuh"
 
