@@ -183,10 +183,13 @@ wrng_gpu_status wrng_gpu_synchronize(wrng_gpu_t* g);
 /* Message of the handle's last failing call ("" when none). */
 const char* wrng_gpu_last_error(const wrng_gpu_t* g);
 /* Pools the shared-memory engine keeps resident at once on cfg->device for
- * fills of this configuration (SMs x CTAs per SM of the fill kernel): a bank
- * of this many pools, or a multiple, runs in whole waves.  0 when the
- * configuration runs on the HBM engine; < 0 (a negated wrng_gpu_status) on
- * error. */
+ * fills of this configuration (SMs x CTAs per SM of the fill kernel x pools
+ * per CTA): a bank of this many pools, or a multiple, runs in whole waves.
+ * For small n = 4 pools (4x256, fp32 4x512: several pools per warp) at
+ * throwaway_f = 1 it is the count that measured fastest, below the occupancy
+ * limit (fills of f = 1 are bound by the number of concurrent output
+ * streams).  0 when the configuration runs on the HBM engine; < 0 (a negated
+ * wrng_gpu_status) on error. */
 int64_t wrng_gpu_resident_pools(const wrng_gpu_config* cfg);
 /* Number of this library's kernels launched by the handle so far. */
 uint64_t wrng_gpu_kernel_launches(const wrng_gpu_t* g);

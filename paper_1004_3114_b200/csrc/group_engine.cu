@@ -104,10 +104,30 @@ __device__ __forceinline__ void sts(uint32_t a, T v) {
         asm volatile("st.shared.f64 [%0+%1], %2;" ::"r"(a), "n"(OFF), "d"(v) : "memory");
 }
 
+// L2 policy of the output copies (0 none, 1 evict_first, 2 evict_last).  With
+// thousands of 4 KiB output streams evict_first measured +2 % (fp32 4x256 R = 1:
+// 78.6-78.9 % against 76.7-77.1 %; evict_last 75.1 %); on C3's 16 KiB refills
+// (smem_impl.cuh) both hints cost 2 % (92.6 % against 94.9 %), so k_smem has none.
+#ifndef WG_EXP_BULK_HINT
+#define WG_EXP_BULK_HINT 1
+#endif
 __device__ __forceinline__ void bulk_store(uint64_t dst, uint32_t src_s, uint32_t bytes) {
+#if WG_EXP_BULK_HINT
+    uint64_t pol;
+#if WG_EXP_BULK_HINT == 1
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#else
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#endif
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                     dst),
+                 "r"(src_s), "r"(bytes), "l"(pol)
+                 : "memory");
+#else
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
                  "r"(src_s), "r"(bytes)
                  : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_commit() {
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -659,9 +679,10 @@ static cudaError_t go(const KernelArgs& a, cudaStream_t st) {
         int ctas = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, kern, 32, S::BYTES);
         // f = 1 fills are bound by the output pattern, not by generation:
-        // fewer, longer output streams measured faster (fp32 4x256: 24 pools per
-        // SM 75.2-76.0 % of the HBM roofline, 32 per SM 73.3 %)
-        if (a.f == 1 && S::MINB > 12 && ctas > 12) ctas = 12;
+        // fewer, longer output streams measured faster — 3/4 of the occupancy
+        // limit (fp32 4x256: 24 pools per SM 76-79 % of the HBM roofline, 32 per
+        // SM 73 %; fp64 4x256: 12 per SM 87.6 %, 16 per SM 83.5 %)
+        if (a.f == 1) ctas = ctas * 3 / 4;
         *static_cast<int*>(a.out) = ctas * (int)S::PPW;
         return e;
     }
@@ -673,13 +694,13 @@ static cudaError_t go(const KernelArgs& a, cudaStream_t st) {
 
 // Shapes the group engine takes (measured against one CTA per pool, one wave
 // of pools each, 2^32 normals, % of the HBM-store roofline):
-// fp32 4x256 f = 1..4: 76 / 53 / 37 / 29 % against 44 / 25 / 18 / 14 %; fp64
-// 4x256 f = 2..4: 62 / 45 / 35 % against 47 / 34 / 26 %; fp64 4x256 at f = 1
-// stays on one CTA per pool (81 % against 80 %: both at the ceiling of the
-// output pattern).
+// fp32 4x256 f = 1..4: 77-79 / 57 / 39 / 30 % against 44 / 25 / 18 / 14 %; fp32
+// 4x512 f = 1, 2: 85 / 50 % against 71 / 39 %; fp64 4x256 f = 1..4: 85-88 / 70 /
+// 49 / 38 % against 81 / 47 / 34 / 26 %.
 bool group_engine_fits(uint32_t n_arrays, uint32_t dtype, uint32_t N, uint32_t f) {
     if (n_arrays != 4) return false;
-    return dtype == WRNG_GPU_F64 ? (N == 256 && f >= 2) : (N == 256 || N == 512);
+    (void)f;
+    return dtype == WRNG_GPU_F64 ? N == 256 : (N == 256 || N == 512);
 }
 
 cudaError_t launch_group(uint32_t dtype, const KernelArgs& a, cudaStream_t st) {
