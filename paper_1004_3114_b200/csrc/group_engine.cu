@@ -1,14 +1,14 @@
-// Group engine: SEVERAL small pools per warp (BASELINE.json configs[4], the
-// 4x256 shapes).  A 4x256 pool gives one warp only 8 columns per thread, so
-// in the one-CTA-per-pool engine (smem_impl.cuh) two thirds of a pass's
-// instructions are its per-pass scalar work (parameter draw, fp64 chi-squared
-// scale, emission bookkeeping).  Here a pool belongs to a GROUP of G = N / J
-// lanes (J = 32 fp32 / 16 fp64 columns per lane, as in C3), a warp carries
-// 32 / G pools side by side, and every lane runs its own pool's scalar work:
-// the fixed cost of a pass is paid once per warp for 4 (fp32) or 2 (fp64)
-// pools.  Groups synchronise with __syncwarp(group mask) only and never
-// depend on one another, so a group whose control flow differs (another
-// matrix variant, an error, one refill more) just diverges for that stretch.
+// Group engine: TWO small pools per warp (BASELINE.json configs[4]: the 4x256
+// shapes, and fp32 4x512).  A 4x256 pool gives one warp only 8 columns per
+// thread, so in the one-CTA-per-pool engine (smem_impl.cuh) two thirds of a
+// pass's instructions are its per-pass scalar work (parameter decode, fp64
+// chi-squared scale, emission bookkeeping).  Here a pool belongs to a GROUP of
+// G = N / J = 16 lanes (J = 16 columns per lane; fp32 4x512: 32), a warp — one
+// CTA — carries 2 pools side by side, and every lane runs its own pool's
+// scalar work: the fixed cost of a pass is paid once per warp for 2 pools.
+// Groups synchronise with __syncwarp(group mask) only and never depend on one
+// another, so a group whose control flow differs (another matrix variant, an
+// error, one refill more) just diverges for that stretch.
 //
 // Same algorithm, state and results as k_smem (bit-identical, tested):
 //   pass            wallace.cpp:113-137 in the modular form (a*j + g) & (N-1)
@@ -25,14 +25,18 @@
 //     state after an error is the reference's;
 //   * the drift audit of a 1024-term pool is the plain sequential loop on
 //     lane 0 of each group (all groups of a warp audit on the same pass);
-//   * full refills leave through the bulk-copy engine from a rotated pool,
-//     16/64-byte aligned spans, exactly as in smem_impl.cuh.
-// Thread-to-column maps (k_group, "thread-to-column map"): chosen per dtype so
-// that the groups of a warp do not collide on shared-memory banks.  Measured
-// alternative (not kept): the 4 fp32 pools of a warp interleaved element by
-// element — conflict-free gathers and stores, but the pool is then no bulk-
-// copy source and per-value warp stores of 32-byte segments cost 4.8 LSU
-// cycles each: 1.49 ms per 2^30 against 1.04 ms with bulk copies.
+//   * the pool is ONE linear image in shared memory (flat index m*N + j at
+//     position m*N + j + rot, rot < 16 bytes), so a full refill leaves as one
+//     bulk copy whose source is 16-byte aligned whatever the output phase;
+//     the < 16 ragged values at either end leave through warp stores;
+//   * thread-to-column maps (k_group, "thread-to-column map") chosen per
+//     dtype so that the groups of a warp do not collide on shared-memory
+//     banks.
+// Measured and not kept: the pools of a warp interleaved
+// element by element (conflict-free, but no bulk-copy source: per-value warp
+// stores of 32-byte segments cost 4.8 LSU cycles each, 1.49 ms per 2^30
+// against 1.04 ms); 4 fp32 pools per warp at 8 warps per SM (64 % of the HBM
+// roofline against 74-79 % for 2 pools per warp at 16 warps per SM).
 // Fills only (unit output of the pool's dtype, no restarts); every other
 // operation on such a handle runs on k_smem over the same device state.
 #include <type_traits>
@@ -53,13 +57,12 @@ template <typename T, int LOGN>
 struct Shape {
     static constexpr uint32_t N = 1u << LOGN;
     static constexpr uint32_t ES = (uint32_t)sizeof(T);
-#ifndef WG_GRP_J256  // fp32 4x256: columns per lane (32: 4 pools per warp; 16: 2 pools, 16 warps/SM)
-#define WG_GRP_J256 16
-#endif
-    static constexpr uint32_t J = ES == 4 ? (LOGN == 8 ? WG_GRP_J256 : 32) : 16;  // columns per lane
+    // columns per lane: 16 (64 data registers fp32, 128 fp64); fp32 4x512: 32.
+    // (fp32 4x256 with J = 32 — 4 pools per warp, 8 warps per SM — measured 64 %.)
+    static constexpr uint32_t J = ES == 4 ? (LOGN == 8 ? 16 : 32) : 16;
     static constexpr uint32_t G = N / J;              // lanes per pool
     static constexpr uint32_t PPW = 32 / G;           // pools per warp
-    static_assert(G >= 8 && G <= 16, "group engine shapes: 2 or 4 pools per warp");
+    static_assert(G == 16 && PPW == 2, "group engine shapes: 2 pools per warp");
     static constexpr uint32_t ABYTES = N * ES;
     // a pool in shared memory: flat index i = m*N + j at position i + rot,
     // rot < VEC (one linear image, so a full refill is ONE bulk copy)
@@ -69,10 +72,9 @@ struct Shape {
     static constexpr uint32_t NVALS = 4 * N;
     static constexpr uint32_t CAP = NVALS - 1;
     static constexpr uint32_t VEC = 16 / ES;
-#ifndef WG_GRP_MINB64  // CTAs per SM the registers must allow at 64 data registers
-#define WG_GRP_MINB64 16
-#endif
-    static constexpr uint32_t MINB = (J * ES <= 64) ? WG_GRP_MINB64 : 8;
+    // CTAs per SM the register budget must allow: 16 at 64 data registers (12
+    // at 166 registers measured 72 % against 74.8 %), else 8
+    static constexpr uint32_t MINB = (J * ES <= 64) ? 16 : 8;
     // fp32: residue-class thread-to-column map (k_group, "thread-to-column map")
     static constexpr bool R4 = ES == 4;
     // shared layout: word buffers | pools

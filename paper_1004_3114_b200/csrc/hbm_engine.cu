@@ -869,6 +869,14 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned l
 #endif
 constexpr uint32_t kRunThreads = 512;
 constexpr uint32_t kRunTile = 64;
+#ifndef WG_RUN_TILE_H
+// k_hbm_run's emission tiles are kRunTile (jl: 512 B output runs) x kRunTileH
+// (jh).  64 x 64 gives C2 1024 tiles = 3.46 per CTA (4 rounds, 86 % balance);
+// 64 x 32 balances better (6.9 per CTA) but doubles the per-tile barriers and
+// index work: C2 8.96 ms per step against 8.74-8.82 ms, so 64 stays.
+#define WG_RUN_TILE_H 64
+#endif
+constexpr uint32_t kRunTileH = WG_RUN_TILE_H;
 constexpr uint32_t kRunStages = 3;  // source-row buffers in flight per CTA
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -957,28 +965,29 @@ __global__ void __launch_bounds__(kRunThreads, 2)
     // tiles claimed from an atomic counter instead of blockIdx-strided.
     auto emit = [&](const T* e_pool, uint64_t e_n, uint64_t e_off, unsigned* ctr) {
         // natural index m*N + jh*C + jl is stored at m*N + jl*R + jh
-        const uint32_t tiles_h = (R + kRunTile - 1) / kRunTile;
+        const uint32_t tiles_h = (R + kRunTileH - 1) / kRunTileH;
         const uint32_t tiles_l = (C + kRunTile - 1) / kRunTile;
         const uint32_t ntiles = tiles_h * tiles_l * NA;
         char* outc = static_cast<char*>(a.out) + e_off * (a.out_f32 ? 4 : 8);
         const uint32_t tx = t & 31u, ty = t >> 5;  // 32 x 16
-        // the next tile's 8 values per thread load while this one is stored
+        // the next tile's values (4 or 8 per thread) load while this one is stored
         auto tile_at = [&](uint32_t tl, uint32_t& m, uint32_t& jh0, uint32_t& jl0) {
             m = tl / (tiles_h * tiles_l);
             const uint32_t rem = tl - m * tiles_h * tiles_l;
-            jh0 = (rem % tiles_h) * kRunTile;
+            jh0 = (rem % tiles_h) * kRunTileH;
             jl0 = (rem / tiles_h) * kRunTile;
         };
-        auto load_tile = [&](uint32_t tl, T (&v)[8]) {
+        constexpr uint32_t HN = kRunTileH / 32;  // 32-wide column groups of a tile
+        auto load_tile = [&](uint32_t tl, T (&v)[4 * HN]) {
             uint32_t m, jh0, jl0;
             tile_at(tl, m, jh0, jl0);
             const T* pool = e_pool + (uint64_t)m * N;
 #pragma unroll
             for (uint32_t k = 0; k < 4; ++k)
 #pragma unroll
-                for (uint32_t h = 0; h < 2; ++h) {
+                for (uint32_t h = 0; h < HN; ++h) {
                     const uint32_t jl = jl0 + ty + 16 * k, jh = jh0 + tx + 32 * h;
-                    v[2 * k + h] = jl < C && jh < R ? pool[(uint64_t)jl * R + jh] : (T)0;
+                    v[HN * k + h] = jl < C && jh < R ? pool[(uint64_t)jl * R + jh] : (T)0;
                 }
         };
         // tiles: static (tl = blockIdx.x + k gridDim.x) or claimed from *ctr
@@ -990,13 +999,13 @@ __global__ void __launch_bounds__(kRunThreads, 2)
         };
         int slot = 0;
         uint32_t tl = ctr ? next(0, slot) : blockIdx.x;
-        T v[8];
+        T v[4 * HN];
         if (tl < ntiles) load_tile(tl, v);
         while (tl < ntiles) {
 #pragma unroll
             for (uint32_t k = 0; k < 4; ++k)
 #pragma unroll
-                for (uint32_t h = 0; h < 2; ++h) tile[ty + 16 * k][tx + 32 * h] = v[2 * k + h];
+                for (uint32_t h = 0; h < HN; ++h) tile[ty + 16 * k][tx + 32 * h] = v[HN * k + h];
             __syncthreads();
             slot ^= 1;
             const uint32_t nt = next(tl, slot);
@@ -1005,7 +1014,7 @@ __global__ void __launch_bounds__(kRunThreads, 2)
             tile_at(tl, m, jh0, jl0);
             const uint64_t mbase = (uint64_t)m * N;
 #pragma unroll
-            for (uint32_t k = 0; k < kRunTile; k += 16) {
+            for (uint32_t k = 0; k < kRunTileH; k += 16) {
                 const uint32_t jh = jh0 + ty + k;
 #pragma unroll
                 for (uint32_t h = 0; h < kRunTile; h += 32) {
