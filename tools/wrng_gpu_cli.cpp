@@ -200,83 +200,119 @@ wrng::WallaceConfig make_config(const Options& o, std::uint64_t seed, std::uint3
     return c;
 }
 
-bool write_text(std::FILE* out, std::span<const double> vals) {
-    for (double v : vals)
-        if (std::fprintf(out, "%.17g\n", v) < 0) return false;
-    return true;
-}
+// Values leave in blocks sized for the GPU path: one device fill and one
+// device-to-host copy per 2^20 normals (the stream is the same for any
+// blocking, WallaceState::fill continues it).
+constexpr size_t kBlockValues = size_t(1) << 20;
 
-bool write_f64le(std::FILE* out, std::span<const double> vals) {
-    std::vector<unsigned char> buf(vals.size() * 8);
-    size_t o = 0;
-    for (double v : vals) {
-        std::uint64_t bits;
-        std::memcpy(&bits, &v, 8);
-        for (int i = 0; i < 8; ++i) buf[o++] = (unsigned char)(bits >> (8 * i));
+// stdout in one of the CLI's two wire formats (proj/tools/main.cpp:59-80
+// defines them): "text" — one "%.17g" per line; anything else — raw
+// little-endian IEEE-754 doubles.  One byte buffer per block, one fwrite.
+class Sink {
+public:
+    explicit Sink(const std::string& format) : text_(format == "text") {}
+
+    // false once stdout stops taking data (closed pipe, full device)
+    bool put(const double* v, size_t n) {
+        bytes_.clear();
+        if (text_) {
+            char line[48];
+            for (size_t i = 0; i < n; ++i) {
+                const int len = std::snprintf(line, sizeof line, "%.17g\n", v[i]);
+                bytes_.insert(bytes_.end(), line, line + len);
+            }
+        } else {
+            bytes_.resize(n * sizeof(double));
+            for (size_t i = 0; i < n; ++i) {
+                std::uint64_t w;
+                std::memcpy(&w, v + i, sizeof w);
+                unsigned char* dst = bytes_.data() + i * sizeof w;
+                for (unsigned k = 0; k < sizeof w; ++k, w >>= 8) dst[k] = (unsigned char)w;
+            }
+        }
+        return std::fwrite(bytes_.data(), 1, bytes_.size(), stdout) == bytes_.size();
     }
-    return std::fwrite(buf.data(), 1, buf.size(), out) == buf.size();
+    bool flush() { return std::fflush(stdout) == 0; }
+
+private:
+    bool text_;
+    std::vector<unsigned char> bytes_;
+};
+
+// The generator a command runs on: restored from --state-file when that file
+// exists, freshly seeded otherwise.  rc != kExitOk: the file was malformed
+// (reported on stderr, exit code of proj/tools/main.cpp:84-100).
+std::unique_ptr<wrng::WallaceState> open_generator(const Options& o, int& rc) {
+    rc = kExitOk;
+    if (!o.state_file.empty()) {
+        std::ifstream f(o.state_file, std::ios::binary);
+        if (f) {
+            const std::vector<std::uint8_t> image{std::istreambuf_iterator<char>(f),
+                                                  std::istreambuf_iterator<char>()};
+            try {
+                return std::make_unique<wrng::WallaceState>(
+                    wrng::WallaceState::load_state(image, o.device));
+            } catch (const wrng::malformed_state_error& e) {
+                std::fprintf(stderr, "wrng-gpu: %s: %s\n", o.state_file.c_str(), e.what());
+                rc = kExitStateFile;
+                return nullptr;
+            }
+        }
+    }
+    return std::make_unique<wrng::WallaceState>(make_config(o, o.seed, o.pools ? o.pools : 1));
 }
 
-bool emit(std::span<const double> vals, const std::string& fmt) {
-    return fmt == "text" ? write_text(stdout, vals) : write_f64le(stdout, vals);
+// Writes the generator's state image back (proj/tools/main.cpp:116-127).
+int close_generator(const Options& o, const wrng::WallaceState& st) {
+    if (o.state_file.empty()) return kExitOk;
+    const auto image = st.save_state();
+    std::ofstream f(o.state_file, std::ios::binary | std::ios::trunc);
+    f.write(reinterpret_cast<const char*>(image.data()), (std::streamsize)image.size());
+    if (f) return kExitOk;
+    std::fprintf(stderr, "wrng-gpu: cannot write %s\n", o.state_file.c_str());
+    return kExitStateFile;
 }
 
 // ---------------------------------------------------------------- gen
 int cmd_gen(const Options& o) {
-    std::unique_ptr<wrng::WallaceState> st;
-    if (!o.state_file.empty()) {  // main.cpp:84-100
-        std::ifstream in(o.state_file, std::ios::binary);
-        if (in) {
-            std::vector<std::uint8_t> bytes((std::istreambuf_iterator<char>(in)),
-                                            std::istreambuf_iterator<char>());
-            try {
-                st = std::make_unique<wrng::WallaceState>(
-                    wrng::WallaceState::load_state(bytes, o.device));
-            } catch (const wrng::malformed_state_error& e) {
-                std::fprintf(stderr, "wrng-gpu: %s: %s\n", o.state_file.c_str(), e.what());
-                return kExitStateFile;
-            }
-        }
+    int rc;
+    const auto st = open_generator(o, rc);
+    if (!st) return rc;
+    Sink sink(o.format);
+    std::vector<double> block((size_t)std::min<std::uint64_t>(o.count, kBlockValues));
+    for (std::uint64_t sent = 0; sent < o.count;) {
+        const size_t n = (size_t)std::min<std::uint64_t>(o.count - sent, block.size());
+        st->fill(std::span<double>(block.data(), n), o.mu, o.sigma);
+        if (!sink.put(block.data(), n)) break;
+        sent += n;
     }
-    if (!st) st = std::make_unique<wrng::WallaceState>(make_config(o, o.seed, o.pools ? o.pools : 1));
-    std::vector<double> buf(1u << 14);
-    for (std::uint64_t left = o.count; left > 0;) {
-        const size_t take = (size_t)std::min<std::uint64_t>(left, buf.size());
-        st->fill(std::span<double>(buf.data(), take), o.mu, o.sigma);
-        if (!emit(std::span<const double>(buf.data(), take), o.format)) break;
-        left -= take;
-    }
-    std::fflush(stdout);
-    if (!o.state_file.empty()) {  // main.cpp:116-127
-        const auto bytes = st->save_state();
-        std::ofstream out(o.state_file, std::ios::binary | std::ios::trunc);
-        out.write(reinterpret_cast<const char*>(bytes.data()), (std::streamsize)bytes.size());
-        if (!out) {
-            std::fprintf(stderr, "wrng-gpu: cannot write %s\n", o.state_file.c_str());
-            return kExitStateFile;
-        }
+    sink.flush();
+    return close_generator(o, *st);
+}
+
+// ---------------------------------------------------------------- stream
+// Until the consumer closes the pipe, which is a clean exit
+// (proj/tools/main.cpp:133-141).
+int cmd_stream(const Options& o) {
+    std::signal(SIGPIPE, SIG_IGN);
+    wrng::WallaceState st(make_config(o, o.seed, o.pools ? o.pools : 1));
+    Sink sink(o.format);
+    std::vector<double> block(kBlockValues);
+    while (true) {
+        st.fill(std::span<double>(block), o.mu, o.sigma);
+        if (!sink.put(block.data(), block.size()) || !sink.flush()) break;
     }
     return kExitOk;
 }
 
-// ---------------------------------------------------------------- stream
-int cmd_stream(const Options& o) {
-    std::signal(SIGPIPE, SIG_IGN);  // main.cpp:133-141
-    wrng::WallaceState st(make_config(o, o.seed, o.pools ? o.pools : 1));
-    std::vector<double> buf(1u << 14);
-    for (;;) {
-        st.fill(std::span<double>(buf), o.mu, o.sigma);
-        if (!emit(buf, o.format)) return kExitOk;
-        if (std::fflush(stdout) != 0) return kExitOk;
-    }
-}
-
 // ---------------------------------------------------------------- test
+// One verdict line per check, in the reference CLI's column layout
+// (proj/tools/main.cpp:147-158), and the counts the summary needs.
 struct Tally {
     int tests = 0, failed = 0;
     void line(const std::string& name, double statistic, const std::string& thr, bool pass) {
-        ++tests;
-        failed += !pass;
+        tests += 1;
+        if (!pass) failed += 1;
         std::printf("%-34s statistic=%-12.5g threshold=%-22s %s\n", name.c_str(), statistic,
                     thr.c_str(), pass ? "PASS" : "FAIL");
     }
