@@ -396,6 +396,9 @@ __global__ void __launch_bounds__(32, Shape<T, LOGN>::MINB) k_group(const Kernel
             wpos += 9;
             --wleft;
             ++nstart;
+            // (every lane runs the fp64 scale chain: on lane 0 of the group with a
+            // broadcast — 1.1 % faster for C3 in smem_impl.cuh — the f >= 2 fills
+            // here lost 3 %, the f = 1 fills nothing)
             double scale = 0.0, target = 0.0;
             if (pass_scale(tracked, withheld, S::NVALS, mode, scale, target)) {
                 err = WRNG_GPU_ECORRUPT;  // wallace.cpp:59-61, after the draws

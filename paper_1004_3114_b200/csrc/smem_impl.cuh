@@ -358,6 +358,9 @@ __device__ __forceinline__ void phase_b2(uint32_t pool_s, uint32_t (&ixb)[4],
     });
 }
 
+#ifndef WG_SCALE_LANE0  // 1: the pass's fp64 scale chain on one lane per warp (power)
+#define WG_SCALE_LANE0 1
+#endif
 #ifndef WG_GATHER_FIRST  // 1: gather all columns, then one small per-variant transform
 #define WG_GATHER_FIRST 1
 #endif
@@ -708,10 +711,29 @@ __device__ __forceinline__ bool smem_pass(uint32_t pool_s, uint32_t mode, uint32
     const uint32_t variant = cp.variant;
     const double tracked = ctl->tracked, withheld = ctl->withheld;
     double scale = 0.0, target = 0.0;
-    const int e = pass_scale(tracked, withheld, (uint32_t)S::NVALS, mode, scale, target);
+    int e = 0;
+    double c0d = 0.0, c1d = 0.0;
+#if WG_SCALE_LANE0
+    // lane 0 of every warp runs the fp64 div/sqrt chain and broadcasts the two
+    // coefficients: the same issue slots, but 1/32 of the fp64 datapath energy
+    T c0 = (T)0, c1 = (T)0;
+    if ((tid & 31u) == 0) {
+        e = pass_scale(tracked, withheld, (uint32_t)S::NVALS, mode, scale, target);
+        // regenerate folds the scale into the matrix (wallace.cpp:116-117)
+        c0d = NA == 2 ? cp.c * scale : (variant ? scale : 0.5 * scale);
+        c1d = NA == 2 ? cp.s * scale : scale;
+        c0 = (T)c0d;  // fp32 pools: rounded once (docs/n4_spec.md §4)
+        c1 = (T)c1d;
+    }
+    e = __shfl_sync(0xffffffffu, e, 0);
+    c0 = __shfl_sync(0xffffffffu, c0, 0);
+    if (NA == 2) c1 = __shfl_sync(0xffffffffu, c1, 0);
+#else
+    e = pass_scale(tracked, withheld, (uint32_t)S::NVALS, mode, scale, target);
     // regenerate folds the scale into the matrix (wallace.cpp:116-117)
-    const double c0d = NA == 2 ? cp.c * scale : (variant ? scale : 0.5 * scale);
-    const double c1d = NA == 2 ? cp.s * scale : scale;
+    c0d = NA == 2 ? cp.c * scale : (variant ? scale : 0.5 * scale);
+    c1d = NA == 2 ? cp.s * scale : scale;
+#endif
     if (e) {  // every thread sees the same e (wallace.cpp:59-61)
         if (tid == 0) ctl->error = e;
         __syncthreads();
@@ -744,7 +766,9 @@ __device__ __forceinline__ bool smem_pass(uint32_t pool_s, uint32_t mode, uint32
     }
     if (prefetch)
         draw_pass_params_all<NA>(&sm_at<uint64_t>(S::TAB_OFF), ctl, N, slot ^ 1, tid < 32);
+#if !WG_SCALE_LANE0
     const T c0 = (T)c0d, c1 = (T)c1d;  // fp32 pools: rounded once (docs/n4_spec.md §4)
+#endif
     double wh = 0.0;
     const uint32_t md = emit_n == 0                                    ? 0u
                         : (EM == EM_UNIT && emit_n == (uint32_t)S::CAP) ? (bulk_on ? 3u : 1u)
