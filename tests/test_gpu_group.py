@@ -291,3 +291,44 @@ def test_group_and_one_cta_per_pool_engines_agree(W, dt, p, f):
         assert r.returncode == 0, r.stderr
         outs.append(r.stdout.strip().splitlines()[-1])
     assert outs[0] == outs[1]
+
+
+def test_group_one_pool_of_a_warp_fails_the_other_completes(W):
+    """The two groups of a warp never wait for one another: when pool 1's audit
+    fails mid-fill, pool 0 (same warp) still completes its whole segment, and
+    both pools end in the states the oracle reaches for them separately."""
+    import torch
+
+    kw = dict(pool_exponent=8, throwaway_f=1, seed=21, n_arrays=4)
+    g = W.WallaceState(W.WallaceConfig(dtype="f32", drift_check_period=4, pools=2,
+                                       init_on_host=True, **kw))
+    o = [O.OracleState(dtype=O.F32, drift_period=4, stream=q, **kw) for q in (0, 1)]
+    cap = 4 * 256 - 1
+    t = torch.full((2 * 9 * cap,), -5.0, dtype=torch.float32, device="cuda:0")
+    g.fill(t[:2 * (cap + 3)])
+    for q in (0, 1):
+        assert_bits(t[q * (cap + 3):(q + 1) * (cap + 3)].cpu().numpy(), o[q].fill(cap + 3))
+    p1 = g.active_pool(1)
+    p1.arrays[2, 5] += 1000.0
+    g.set_active_pool(p1, 1)
+    ov, ot, ow = o[1].pool()
+    ov[2 * 256 + 5] += 1000.0
+    o[1].set_pool(ov, ot, ow)
+    per = 9 * cap
+    with pytest.raises(W.CorruptedStateError):
+        g.fill(t)
+        g.synchronize()
+    assert_bits(t[:per].cpu().numpy(), o[0].fill(per))      # pool 0: the whole segment
+    with pytest.raises(O.OracleError):
+        o[1].fill(per)
+    for q in (0, 1):
+        oc = o[q].counters()
+        assert (g.pass_count(q), g.avail(q)) == (oc["pass_count"], oc["avail"]), q
+        tb, r, s_, d = o[q].uniform()
+        us = g.uniform_state(q)
+        assert_bits(us.lag_table, tb)
+        assert (us.cursor_r, us.draws) == (r, d)
+        pv, pt, pw = o[q].pool()
+        gp = g.active_pool(q)
+        assert_bits(gp.arrays.reshape(-1), pv)
+        assert (gp.tracked_sumsq, gp.withheld) == (pt, pw)
