@@ -65,8 +65,10 @@ extern __shared__ __align__(16) unsigned char g_sm[];
 // emitted value (wrng_gpu_validate: s1..s4 fused into the emitting pass)
 enum EmitMode : int { EM_UNIT = 0, EM_GENERIC = 1, EM_STATS = 2 };
 
-#ifndef WG_RBUDGET_MIN  // smallest per-thread register budget of a shape (128 measured slower:
-                        // 4x256 pools 32 % vs 37.5 % fp32, 66 % vs 81 % fp64)
+#ifndef WG_RBUDGET_MIN  // smallest per-thread register budget of a shape.  255 here: the
+                        // f = 1 fills of small pools are bound by their output pattern and
+                        // ran best at 8 CTAs per SM (fp64 4x256: 82 % at 8, 70 % at 16); the
+                        // f >= 2 engine (smem_r64.cu) sets 128 for 16 warps per SM
 #define WG_RBUDGET_MIN 255
 #endif
 
@@ -90,8 +92,7 @@ struct SmemShape {
     static constexpr uint32_t NTH = N / J;                                         // CTA size
     // CTAs per SM the register budget must allow: twice the data registers
     // J * (regs per column), at least WG_RBUDGET_MIN and at most 255 per
-    // thread (C3: 32 threads x 8 CTAs).  A 4x256 pool could run 16 CTAs per
-    // SM at 128 registers, but measured slower than 8 at 255.
+    // thread (C3: 32 threads x 8 CTAs).
     static constexpr uint32_t DATA = J * (NA * (uint32_t)sizeof(T) / 4);
     static constexpr uint32_t RBUDGET = 2 * DATA > 255                ? 255
                                         : 2 * DATA < WG_RBUDGET_MIN ? WG_RBUDGET_MIN
