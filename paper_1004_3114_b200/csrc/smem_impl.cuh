@@ -94,7 +94,20 @@ struct SmemShape {
     // J * (regs per column), at least WG_RBUDGET_MIN and at most 255 per
     // thread (C3: 32 threads x 8 CTAs).
     static constexpr uint32_t DATA = J * (NA * (uint32_t)sizeof(T) / 4);
-    static constexpr uint32_t RBUDGET = 2 * DATA > 255                ? 255
+    // fp32 pools of >= 2 warps with 128 data registers (4x2048, 4x4096): as many
+    // CTAs per SM as shared memory holds, the register budget cut to match —
+    // f = 1 fills overlap one CTA's emission with the others' passes, and 2
+    // CTAs per SM left the SM idle while both waited for their bulk copies
+    // (4x4096: 3 CTAs per SM at 168 registers 87.3 % of the HBM roofline
+    // against 80.7 % at 2; 4x2048: 5 at 200 registers 90.5 % against 89.0 %;
+    // the fp64 shapes, at 95 %, gain nothing: 4x1024 91.8 % at 5 against 96.2 %)
+    static constexpr uint32_t POOLB = NA * N * (uint32_t)sizeof(T);
+    static constexpr uint32_t SMEM_CTAS = (227u * 1024u) / (POOLB + 9u * 1024u);
+    static constexpr uint32_t RB_OCC = SMEM_CTAS ? (65536u / (NTH * SMEM_CTAS)) & ~7u : 255u;
+    static constexpr bool OCC_TUNE = sizeof(T) == 4 && NTH >= 64 && 2 * DATA > 255 &&
+                                     RB_OCC < 255 && RB_OCC >= DATA + 30;
+    static constexpr uint32_t RBUDGET = OCC_TUNE                      ? RB_OCC
+                                        : 2 * DATA > 255             ? 255
                                         : 2 * DATA < WG_RBUDGET_MIN ? WG_RBUDGET_MIN
                                                                       : 2 * DATA;
     static constexpr uint32_t MINB_R = 65536 / (NTH * RBUDGET);
