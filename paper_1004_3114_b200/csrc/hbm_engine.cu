@@ -23,29 +23,37 @@
 namespace wg {
 
 // ---------------------------------------------------------------------------
-// pass parameters: one warp draws the uniform-generator part of `npass`
-// consecutive passes; the scale needs the previous pass's withheld value and
-// is derived inside each pass kernel.
+// pass parameters: the uniform-generator part of `npass` consecutive passes;
+// the scale needs the previous pass's withheld value and is derived inside
+// each pass kernel.  One CTA: the words of up to kParTile passes are produced
+// in one parallel table step (x[i] += x[i+334] is hazard-free for 273
+// consecutive words, common.cuh), then one thread per pass decodes its words
+// (draw order of wallace.cpp:54-58).  (One warp drawing pass after pass took
+// 29 us per 64-pass batch, 3 % of a C2 step.)
 // ---------------------------------------------------------------------------
+constexpr uint32_t kParThreads = 256;
 template <int NA>
-__global__ void k_hbm_params(uint32_t N, LfgState* lfg, wrng_gpu_params* params,
-                             uint32_t npass, PoolMeta* meta) {
-    constexpr int K = NA == 2 ? 6 : 9;
+__global__ void __launch_bounds__(kParThreads)
+    k_hbm_params(uint32_t N, LfgState* lfg, wrng_gpu_params* params, uint32_t npass,
+                 PoolMeta* meta) {
+    constexpr uint32_t K = NA == 2 ? 6 : 9;
+    constexpr uint32_t kParTile = 252 / K;  // passes per table step (<= 256 words)
     __shared__ uint64_t tab[kTable];
-    __shared__ uint64_t w[32];
+    __shared__ uint64_t w[kParTile * K];
     LfgState* lg = lfg + blockIdx.x;
     if (meta[blockIdx.x].error) return;
-    for (uint32_t i = threadIdx.x; i < kTable; i += 32) tab[i] = lg->table[i];
+    const uint32_t t = threadIdx.x;
+    for (uint32_t i = t; i < kTable; i += kParThreads) tab[i] = lg->table[i];
     uint32_t r = lg->r;
-    __syncwarp();
-    for (uint32_t ps = 0; ps < npass; ++ps) {
-        if (threadIdx.x < K) w[threadIdx.x] = lfg_word_at(tab, r, threadIdx.x);
-        __syncwarp();
-        r += K;
-        r = r >= kTable ? r - kTable : r;
-        if (threadIdx.x == 0) {
+    __syncthreads();
+    for (uint32_t ps0 = 0; ps0 < npass; ps0 += kParTile) {
+        const uint32_t np = npass - ps0 < kParTile ? npass - ps0 : kParTile;
+        if (t < np * K) w[t] = lfg_word_at(tab, r, t);
+        r = (r + np * K) % kTable;
+        __syncthreads();
+        if (t < np) {
             LfgParams lp;
-            lfg_params<NA>(w, N, lp);
+            lfg_params<NA>(w + t * K, N, lp);
             wrng_gpu_params p;
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
@@ -58,12 +66,12 @@ __global__ void k_hbm_params(uint32_t N, LfgState* lfg, wrng_gpu_params* params,
             p.s = lp.s;
             p.scale = 0.0;
             p.target_sumsq = 0.0;
-            params[(uint64_t)blockIdx.x * npass + ps] = p;
+            params[(uint64_t)blockIdx.x * npass + ps0 + t] = p;
         }
-        __syncwarp();
+        __syncthreads();
     }
-    for (uint32_t i = threadIdx.x; i < kTable; i += 32) lg->table[i] = tab[i];
-    if (threadIdx.x == 0) {
+    for (uint32_t i = t; i < kTable; i += kParThreads) lg->table[i] = tab[i];
+    if (t == 0) {
         lg->r = r;
         lg->draws += (uint64_t)K * npass;
     }
@@ -73,9 +81,9 @@ cudaError_t launch_hbm_params(uint32_t n_arrays, uint32_t N, LfgState* lfg,
                               wrng_gpu_params* params, uint32_t npass, PoolMeta* meta,
                               cudaStream_t st) {
     if (n_arrays == 2)
-        k_hbm_params<2><<<1, 32, 0, st>>>(N, lfg, params, npass, meta);
+        k_hbm_params<2><<<1, kParThreads, 0, st>>>(N, lfg, params, npass, meta);
     else
-        k_hbm_params<4><<<1, 32, 0, st>>>(N, lfg, params, npass, meta);
+        k_hbm_params<4><<<1, kParThreads, 0, st>>>(N, lfg, params, npass, meta);
     return cudaGetLastError();
 }
 
@@ -371,12 +379,34 @@ __device__ __forceinline__ double pool_term(const T* v, uint64_t i, uint32_t N,
     return sq_term(v[hbm_pos(i, N, sp)]);
 }
 
+// Which chunk of its CTA's kSumCta consecutive chunks thread t evaluates.  A
+// chunk is kSumChunk consecutive natural indices jh*C + jl .. (one jh, a run
+// of jl), stored kSumChunk rows apart — storage position jl*R + jh — so with
+// thread = chunk a warp's load touches 32 rows: 32 sectors for 256 bytes.
+// When a natural row holds CPR = C / kSumChunk whole chunks and the CTA covers
+// JH = kSumCta / CPR whole rows, thread t takes chunk (t % JH) * CPR + t / JH:
+// JH consecutive lanes then read JH consecutive jh of one storage row (64
+// contiguous bytes for C2's JH = 8; a quarter of the sectors).  The results
+// change hands through shared memory, so everything after the term loops
+// (the scan, the 32-chunk compositions, the stores) stays in natural order.
+__device__ __forceinline__ uint32_t sum_chunk_of_thread(uint32_t t, uint32_t N) {
+    const HbmSplit sp = hbm_split(N);
+    const uint32_t C = 1u << sp.lc;
+    const uint32_t cpr = C / kSumChunk;
+    if (cpr < 1 || C % kSumChunk || cpr * 2 > kSumCta || kSumCta % cpr ||
+        (N / kSumChunk) % kSumCta)
+        return t;
+    const uint32_t jhn = kSumCta / cpr;
+    return (t % jhn) * cpr + t / jhn;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kSumCta) k_sum_chunks(KernelArgs a, uint32_t buf,
                                                         uint64_t nvals, double* pre_local,
                                                         double* cta_sum, uint32_t nch) {
     __shared__ double part[kSumCta];
-    const uint32_t t = threadIdx.x, c = blockIdx.x * kSumCta + t;
+    const uint32_t t = threadIdx.x;
+    const uint32_t cl = sum_chunk_of_thread(t, a.N), c = blockIdx.x * kSumCta + cl;
     const T* v = static_cast<const T*>(a.buf[buf]);
     const HbmSplit sp = hbm_split(a.N);
     double s = 0.0;
@@ -384,7 +414,7 @@ __global__ void __launch_bounds__(kSumCta) k_sum_chunks(KernelArgs a, uint32_t b
         const uint64_t lo = (uint64_t)c * kSumChunk, hi = umin64(lo + kSumChunk, nvals);
         for (uint64_t i = lo; i < hi; ++i) s += pool_term(v, i, a.N, sp);
     }
-    part[t] = s;
+    part[cl] = s;
     __syncthreads();
     for (uint32_t off = 1; off < kSumCta; off <<= 1) {  // inclusive scan (approximate)
         const double x = t >= off ? part[t - off] : 0.0;
@@ -392,7 +422,8 @@ __global__ void __launch_bounds__(kSumCta) k_sum_chunks(KernelArgs a, uint32_t b
         part[t] += x;
         __syncthreads();
     }
-    if (c < nch) pre_local[c] = part[t] - s;
+    // thread t now writes chunk t's exclusive prefix
+    if (blockIdx.x * kSumCta + t < nch) pre_local[blockIdx.x * kSumCta + t] = t ? part[t - 1] : 0.0;
     if (t == kSumCta - 1) cta_sum[blockIdx.x] = part[t];
 }
 
@@ -402,7 +433,9 @@ __global__ void __launch_bounds__(kSumCta) k_sum_segs(KernelArgs a, uint32_t buf
                                                       const double* cta_sum, SumSeg* segs,
                                                       SumSeg* blocks, uint32_t nch) {
     __shared__ double s_base;
-    const uint32_t t = threadIdx.x, c = blockIdx.x * kSumCta + t;
+    __shared__ SumSeg s_seg[kSumCta];
+    const uint32_t t = threadIdx.x;
+    const uint32_t cl = sum_chunk_of_thread(t, a.N);
     if (t < 32) {  // prefix of the previous CTAs' sums (approximate)
         double x = 0.0;
         for (uint32_t b = t; b < blockIdx.x; b += 32) x += cta_sum[b];
@@ -413,17 +446,25 @@ __global__ void __launch_bounds__(kSumCta) k_sum_segs(KernelArgs a, uint32_t buf
     __syncthreads();
     const T* v = static_cast<const T*>(a.buf[buf]);
     const HbmSplit sp = hbm_split(a.N);
-    const double pre = c < nch ? s_base + pre_local[c] : 0.0;
-    const int e = pre > 0.0 ? exp2_of(pre) : -2000;
-    SumSeg g;
-    seg_init(g, e);
-    if (c < nch && e > -1000) {
-        const double sc = pow2d(52 - e);
-        const uint64_t lo = (uint64_t)c * kSumChunk, hi = umin64(lo + kSumChunk, nvals);
-        for (uint64_t i = lo; i < hi; ++i) seg_push(g, pool_term(v, i, a.N, sp), sc);
-    } else {
-        g.valid = 0;
+    {
+        const uint32_t c = blockIdx.x * kSumCta + cl;  // the chunk this thread evaluates
+        const double pre = c < nch ? s_base + pre_local[c] : 0.0;
+        const int e = pre > 0.0 ? exp2_of(pre) : -2000;
+        SumSeg g;
+        seg_init(g, e);
+        if (c < nch && e > -1000) {
+            const double sc = pow2d(52 - e);
+            const uint64_t lo = (uint64_t)c * kSumChunk, hi = umin64(lo + kSumChunk, nvals);
+            for (uint64_t i = lo; i < hi; ++i) seg_push(g, pool_term(v, i, a.N, sp), sc);
+        } else {
+            g.valid = 0;
+        }
+        s_seg[cl] = g;
     }
+    __syncthreads();
+    // from here thread t holds chunk t (natural order)
+    const uint32_t c = blockIdx.x * kSumCta + t;
+    SumSeg g = s_seg[t];
     if (c < nch) {
         SumSeg f = g;
         seg_finalize(f);
