@@ -455,7 +455,17 @@ __global__ void __launch_bounds__(kSumCta) k_sum_segs(KernelArgs a, uint32_t buf
         if (c < nch && e > -1000) {
             const double sc = pow2d(52 - e);
             const uint64_t lo = (uint64_t)c * kSumChunk, hi = umin64(lo + kSumChunk, nvals);
-            for (uint64_t i = lo; i < hi; ++i) seg_push(g, pool_term(v, i, a.N, sp), sc);
+            // the terms 16 at a time: the loads of a batch are in flight together
+            // (seg_push branches, so the compiler does not hoist them itself)
+            for (uint64_t i0 = lo; i0 < hi; i0 += 16) {
+                double tm[16];
+#pragma unroll
+                for (uint32_t k = 0; k < 16; ++k)
+                    tm[k] = i0 + k < hi ? pool_term(v, i0 + k, a.N, sp) : 0.0;
+#pragma unroll
+                for (uint32_t k = 0; k < 16; ++k)
+                    if (i0 + k < hi) seg_push(g, tm[k], sc);
+            }
         } else {
             g.valid = 0;
         }
