@@ -407,10 +407,13 @@ __device__ __forceinline__ SumSeg seg_compose(const SumSeg& a, const SumSeg& b) 
     SumSeg c;
     c.e = a.e;
     c.valid = a.valid & b.valid & (a.e == b.e ? 1u : 0u);
+    // (selects, not b.s[a.par[h]]: a dynamically indexed member array sends the
+    // whole struct to local memory)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-        c.s[h] = a.s[h] + b.s[a.par[h]];
-        c.par[h] = b.par[a.par[h]];
+        const bool odd = a.par[h] != 0;
+        c.s[h] = a.s[h] + (odd ? b.s[1] : b.s[0]);
+        c.par[h] = odd ? b.par[1] : b.par[0];
     }
     return c;
 }
@@ -430,7 +433,8 @@ __device__ __forceinline__ void seg_finalize(SumSeg& g) {
 __device__ __forceinline__ bool seg_apply(double& q, const SumSeg& g) {
     if (!g.valid || !(q > 0.0) || exp2_of(q) != g.e) return false;
     const double Q = q * pow2d(52 - g.e);
-    const double Qn = Q + __longlong_as_double(g.s[__double_as_longlong(Q) & 1]);
+    const double Qn =
+        Q + __longlong_as_double((__double_as_longlong(Q) & 1) ? g.s[1] : g.s[0]);
     if (!(Qn < 0x1.0p53)) return false;
     q = Qn * pow2d(g.e - 52);
     return true;
