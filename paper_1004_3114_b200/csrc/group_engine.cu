@@ -687,7 +687,8 @@ static cudaError_t go(const KernelArgs& a, cudaStream_t st) {
         // fewer, longer output streams measured faster — 3/4 of the occupancy
         // limit (fp32 4x256: 24 pools per SM 76-79 % of the HBM roofline, 32 per
         // SM 73 %; fp64 4x256: 12 per SM 87.6 %, 16 per SM 83.5 %)
-        if (a.f == 1) ctas = ctas * 3 / 4;
+        // (4x256 only: fp32 4x512 runs 83.5 % with all 16 pools per SM, 76 % with 12)
+        if (a.f == 1 && S::N == 256) ctas = ctas * 3 / 4;
         *static_cast<int*>(a.out) = ctas * (int)S::PPW;
         return e;
     }
